@@ -1,0 +1,121 @@
+// device.cuh — device-resident CSR replica, preprocessing and scratch arenas.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "graph_host.hpp"
+
+#define ADSB_CUDA(call)                                                                     \
+    do {                                                                                    \
+        cudaError_t _e = (call);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            ::adsb::fail(ADSB_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+namespace adsb {
+
+// RAII device allocation.
+template <class T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        reset();
+        ptr = o.ptr;
+        count = o.count;
+        o.ptr = nullptr;
+        o.count = 0;
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void alloc(size_t n) {
+        reset();
+        if (n == 0) n = 1;
+        ADSB_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+        count = n;
+    }
+    void reset() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        count = 0;
+    }
+    size_t bytes() const { return count * sizeof(T); }
+};
+
+// Pinned host staging.
+template <class T>
+struct PinnedBuf {
+    T* ptr = nullptr;
+    size_t count = 0;
+    PinnedBuf() = default;
+    explicit PinnedBuf(size_t n) {
+        if (n == 0) n = 1;
+        ADSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+        count = n;
+    }
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (ptr) cudaFreeHost(ptr);
+    }
+};
+
+struct DeviceGraph {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t nnz = 0;
+    DevBuf<uint32_t> offsets;  // n+1 (nnz < 2^32 on the device path)
+    DevBuf<uint32_t> nbrs;     // nnz
+};
+
+// Per-(graph, device) sampler scratch: one "slot" per concurrently running
+// sample team. Each slot holds per-vertex state (16 B), a visit queue with
+// the visited vertices' CSR ranges, and the t-side level boundaries.
+struct SamplerArena {
+    uint32_t slots = 0;
+    uint32_t n = 0;
+    uint32_t level_cap = 0;
+    DevBuf<unsigned long long> state;  // slots * n * 2 (meta, sigma)
+    DevBuf<uint32_t> queue;            // slots * n
+    DevBuf<uint2> qrange;              // slots * n (offset, degree)
+    DevBuf<uint32_t> tlev;             // slots * level_cap
+    DevBuf<uint32_t> slot_tag;         // slots
+};
+
+struct DeviceContext {
+    int device = 0;
+    DeviceGraph graph;
+    DevBuf<uint32_t> labels;  // component labels (reference numbering)
+    bool labels_ready = false;
+    uint32_t num_components = 0;
+    std::unique_ptr<SamplerArena> arena;
+    cudaStream_t stream = nullptr;   // sampling stream
+    cudaStream_t stream2 = nullptr;  // check / collective stream
+    ~DeviceContext();
+};
+
+int resolve_device(int requested);
+std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int device);
+
+// graph.hpp:153-175 connected_components: labels numbered by smallest member
+// (exactly the reference's numbering); returns the component count.
+uint32_t device_components(DeviceContext& ctx);
+// graph.hpp:178-197 eccentricity
+uint64_t device_eccentricity(DeviceContext& ctx, uint32_t source);
+// graph.hpp:202-214 diameter_upper_bound (requires device_components first)
+uint64_t device_diameter_bound(DeviceContext& ctx);
+
+int num_sms(int device);
+
+}  // namespace adsb

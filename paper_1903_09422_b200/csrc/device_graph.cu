@@ -1,0 +1,269 @@
+// device_graph.cu — device CSR replica and the preprocessing kernels
+// (K5 cc_label, K6 bfs_level, argmax degree) that replace, on the GPU,
+//   graph.hpp:153-175 connected_components
+//   graph.hpp:178-197 eccentricity
+//   graph.hpp:202-214 diameter_upper_bound
+// (paths relative to /root/reference/proj/include/adsamp/).
+//
+// Components: lock-free union-find hooking (larger root -> smaller root), so
+// every root is its component's smallest vertex; ranking the roots in id
+// order then reproduces the reference's DFS numbering exactly.
+// D_ub: one multi-source, level-synchronous BFS from every component's
+// max-degree vertex (lowest id on ties); the deepest level is the largest
+// eccentricity, D_ub = 2 * that.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "device.cuh"
+
+namespace adsb {
+
+namespace {
+
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t uf_root(uint32_t* parent, uint32_t v) {
+    volatile uint32_t* p = parent;
+    uint32_t cur = p[v];
+    if (cur != v) {
+        uint32_t prev = v, next;
+        while (cur > (next = p[cur])) {  // path halving; parents only decrease
+            p[prev] = next;
+            prev = cur;
+            cur = next;
+        }
+    }
+    return cur;
+}
+
+__global__ void uf_init(uint32_t* parent, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        parent[v] = v;
+}
+
+// one warp per vertex, lanes over its neighbours; each undirected edge once (u < w)
+__global__ void uf_hook(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs,
+                        uint32_t* parent, uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = warp; u < n; u += nwarps) {
+        const uint32_t b = off[u], e = off[u + 1];
+        for (uint32_t i = b + lane; i < e; i += 32) {
+            const uint32_t w = nbrs[i];
+            if (w < u) continue;
+            uint32_t ru = uf_root(parent, u), rw = uf_root(parent, w);
+            while (ru != rw) {
+                const uint32_t hi = max(ru, rw), lo = min(ru, rw);
+                const uint32_t old = atomicCAS(&parent[hi], hi, lo);
+                if (old == hi) break;
+                ru = uf_root(parent, old);
+                rw = uf_root(parent, lo);
+            }
+        }
+    }
+}
+
+__global__ void uf_compress(uint32_t* parent, uint32_t* is_root, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t r = uf_root(parent, v);
+        parent[v] = r;
+        is_root[v] = r == v ? 1u : 0u;
+    }
+}
+
+__global__ void uf_label(const uint32_t* parent, const uint32_t* root_rank, uint32_t* label, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        label[v] = root_rank[parent[v]];
+}
+
+// graph.hpp:208: start = max degree, lowest id on ties -> max of (deg, ~v)
+__global__ void argmax_degree(const uint32_t* __restrict__ off, const uint32_t* __restrict__ label,
+                              unsigned long long* best, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const unsigned long long key =
+            (static_cast<unsigned long long>(off[v + 1] - off[v]) << 32) | static_cast<uint32_t>(~v);
+        atomicMax(&best[label[v]], key);
+    }
+}
+
+__global__ void seed_sources(const unsigned long long* best, uint32_t comps, uint32_t* dist,
+                             uint32_t* frontier, uint32_t* count0) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < comps; c += gridDim.x * blockDim.x) {
+        const uint32_t s = ~static_cast<uint32_t>(best[c] & 0xFFFFFFFFull);
+        dist[s] = 0;
+        frontier[c] = s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count0 = comps;
+}
+
+__global__ void init_dist(uint32_t* dist, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        dist[v] = kInf;
+}
+
+// K6: one level of a (multi-source) BFS; warp per frontier vertex.
+__global__ void bfs_level(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs,
+                          uint32_t* dist, const uint32_t* __restrict__ fin, const uint32_t* cnt_in,
+                          uint32_t* fout, uint32_t* cnt_out, uint32_t level) {
+    const uint32_t count = *cnt_in;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = warp; i < count; i += nwarps) {
+        const uint32_t u = fin[i];
+        const uint32_t b = off[u], e = off[u + 1];
+        for (uint32_t j = b + lane; j < e; j += 32) {
+            const uint32_t w = nbrs[j];
+            if (dist[w] == kInf && atomicCAS(&dist[w], kInf, level + 1) == kInf)
+                fout[atomicAdd(cnt_out, 1u)] = w;
+        }
+    }
+}
+
+}  // namespace
+
+int num_sms(int device) {
+    int v = 0;
+    ADSB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    return v;
+}
+
+int resolve_device(int requested) {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        fail(ADSB_ERR_CUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                "); the adsb engine has no CPU fallback");
+    int dev = requested;
+    if (dev < 0) ADSB_CUDA(cudaGetDevice(&dev));
+    if (dev >= count) invalid("CUDA device ordinal out of range");
+    return dev;
+}
+
+DeviceContext::~DeviceContext() {
+    if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
+}
+
+std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int device) {
+    if (g.nnz() >= 0xFFFFFFFFull) invalid("device CSR needs fewer than 2^32 adjacency entries");
+    ADSB_CUDA(cudaSetDevice(device));
+    auto ctx = std::make_unique<DeviceContext>();
+    ctx->device = device;
+    ADSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ADSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    DeviceGraph& dg = ctx->graph;
+    dg.device = device;
+    dg.n = g.n;
+    dg.nnz = g.nnz();
+    // u32 offsets on the device: narrow on the host, then one copy each.
+    std::vector<uint32_t> off32(g.offsets.size());
+    for (size_t i = 0; i < off32.size(); ++i) off32[i] = static_cast<uint32_t>(g.offsets[i]);
+    dg.offsets.alloc(off32.size());
+    dg.nbrs.alloc(std::max<uint64_t>(1, g.nnz()));
+    ADSB_CUDA(cudaMemcpyAsync(dg.offsets.ptr, off32.data(), off32.size() * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    if (g.nnz())
+        ADSB_CUDA(cudaMemcpyAsync(dg.nbrs.ptr, g.nbrs.data(), g.nnz() * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+    ADSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return ctx;
+}
+
+static unsigned grid_for(uint64_t work, int device, unsigned block = 256) {
+    const uint64_t want = (work + block - 1) / block;
+    const uint64_t cap = static_cast<uint64_t>(num_sms(device)) * 8;
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+uint32_t device_components(DeviceContext& ctx) {
+    if (ctx.labels_ready) return ctx.num_components;
+    const uint32_t n = ctx.graph.n;
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint32_t> parent(n), is_root(n), rank(n + 1);
+    ctx.labels.alloc(n);
+    const unsigned g = grid_for(n, ctx.device);
+    uf_init<<<g, 256, 0, s>>>(parent.ptr, n);
+    uf_hook<<<grid_for(static_cast<uint64_t>(n) * 32, ctx.device), 256, 0, s>>>(
+        ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent.ptr, n);
+    uf_compress<<<g, 256, 0, s>>>(parent.ptr, is_root.ptr, n);
+    size_t temp_bytes = 0;
+    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, is_root.ptr, rank.ptr, n + 1, s));
+    DevBuf<uint8_t> temp(temp_bytes);
+    // rank has n+1 entries: scanning n+1 inputs reads is_root[n]; give it a zero tail
+    DevBuf<uint32_t> flags(n + 1);
+    ADSB_CUDA(cudaMemsetAsync(flags.ptr + n, 0, sizeof(uint32_t), s));
+    ADSB_CUDA(cudaMemcpyAsync(flags.ptr, is_root.ptr, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(temp.ptr, temp_bytes, flags.ptr, rank.ptr, n + 1, s));
+    uf_label<<<g, 256, 0, s>>>(parent.ptr, rank.ptr, ctx.labels.ptr, n);
+    uint32_t comps = 0;
+    ADSB_CUDA(cudaMemcpyAsync(&comps, rank.ptr + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ADSB_CUDA(cudaStreamSynchronize(s));
+    ADSB_CUDA(cudaGetLastError());
+    ctx.num_components = comps;
+    ctx.labels_ready = true;
+    return comps;
+}
+
+// Level-synchronous BFS from `sources` (already written into frontier A with
+// dist 0); returns the deepest non-empty level. Levels are launched in
+// chunks so the host synchronises once per chunk, not once per level.
+static uint64_t bfs_depth(DeviceContext& ctx, DevBuf<uint32_t>& dist, DevBuf<uint32_t>& fa,
+                          DevBuf<uint32_t>& fb, DevBuf<uint32_t>& counts) {
+    const uint32_t n = ctx.graph.n;
+    cudaStream_t s = ctx.stream;
+    const unsigned grid = static_cast<unsigned>(num_sms(ctx.device) * 8);
+    constexpr uint32_t kChunk = 32;
+    uint32_t level = 0;
+    std::vector<uint32_t> host(kChunk);
+    for (;;) {
+        for (uint32_t k = 0; k < kChunk && level + k + 1 <= n; ++k) {
+            const uint32_t L = level + k;
+            uint32_t* fin = (L & 1) ? fb.ptr : fa.ptr;
+            uint32_t* fout = (L & 1) ? fa.ptr : fb.ptr;
+            bfs_level<<<grid, 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, dist.ptr, fin,
+                                           counts.ptr + L, fout, counts.ptr + L + 1, L);
+        }
+        const uint32_t avail = std::min<uint32_t>(kChunk, n - level);
+        ADSB_CUDA(cudaMemcpyAsync(host.data(), counts.ptr + level + 1, avail * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, s));
+        ADSB_CUDA(cudaStreamSynchronize(s));
+        ADSB_CUDA(cudaGetLastError());
+        for (uint32_t k = 0; k < avail; ++k)
+            if (host[k] == 0) return level + k;
+        level += avail;
+        if (level >= n) return level;
+    }
+}
+
+uint64_t device_eccentricity(DeviceContext& ctx, uint32_t source) {
+    const uint32_t n = ctx.graph.n;
+    if (source >= n) invalid("source vertex out of range");
+    cudaStream_t s = ctx.stream;
+    DevBuf<uint32_t> dist(n), fa(n), fb(n), counts(static_cast<size_t>(n) + 2);
+    ADSB_CUDA(cudaMemsetAsync(counts.ptr, 0, counts.bytes(), s));
+    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist.ptr, n);
+    const uint32_t zero = 0, one = 1;
+    ADSB_CUDA(cudaMemcpyAsync(dist.ptr + source, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaMemcpyAsync(fa.ptr, &source, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaMemcpyAsync(counts.ptr, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    return bfs_depth(ctx, dist, fa, fb, counts);
+}
+
+uint64_t device_diameter_bound(DeviceContext& ctx) {
+    const uint32_t n = ctx.graph.n;
+    const uint32_t comps = device_components(ctx);
+    cudaStream_t s = ctx.stream;
+    DevBuf<unsigned long long> best(comps);
+    DevBuf<uint32_t> dist(n), fa(n), fb(n), counts(static_cast<size_t>(n) + 2);
+    ADSB_CUDA(cudaMemsetAsync(best.ptr, 0, best.bytes(), s));
+    ADSB_CUDA(cudaMemsetAsync(counts.ptr, 0, counts.bytes(), s));
+    argmax_degree<<<grid_for(n, ctx.device), 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.labels.ptr, best.ptr, n);
+    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist.ptr, n);
+    seed_sources<<<grid_for(comps, ctx.device), 256, 0, s>>>(best.ptr, comps, dist.ptr, fa.ptr, counts.ptr);
+    return 2 * bfs_depth(ctx, dist, fa, fb, counts);
+}
+
+}  // namespace adsb

@@ -1,0 +1,566 @@
+// engine.cu — estimate_bc on the device (kadabra.hpp:308-348) with two
+// pipelines (paths relative to /root/reference/proj/include/adsamp/):
+//
+// Deterministic (indexed-frame, engine.hpp:490-643). Frame p holds spf
+// samples from stream_rng(seed, p). A batch of frames is sampled at once
+// (K1); every interior vertex becomes an event (v << 32 | frame). K4, the
+// ordered cutoff, sorts the events by (v, frame), turns each into "count of v
+// after this frame", takes per-frame maxima and a running max over frames,
+// and evaluates the stopping rule after EVERY frame in position order; the
+// first passing frame P stops the run and only frames <= P are folded. With
+// uniform deltas kadabra_converged (kadabra.hpp:133-144) holds iff f and g
+// pass at the maximum count, because both are monotone in b under IEEE
+// round-to-nearest; the device evaluates them with explicit _rn intrinsics in
+// the reference's expression order (no FMA contraction). Result: tau, data,
+// check_cycles bit-identical to run_indexed at any thread/GPU count.
+//
+// Epoch (non-det variants, cumulative semantics as run_barrier,
+// engine.hpp:267-341). Sample i draws from stream_rng(seed, i); epoch e holds
+// samples [eB, (e+1)B). The sampler (K2) for epoch e+1 runs on stream 1 into
+// count[(e+1)&1] while K3 folds count[e&1] into the running total, zeroes it
+// and checks the rule on stream 2 (after an NCCL all-reduce when several GPUs
+// share the epoch). The run stops at the first epoch whose cumulative state
+// passes (the reference's run_epoch checks one epoch only, a defect we do not
+// reproduce).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "comm.hpp"
+#include "engine.hpp"
+#include "sampler.cuh"
+
+namespace adsb {
+
+// ---------------------------------------------------------------------------
+// Scalar rules (host)
+// ---------------------------------------------------------------------------
+uint64_t compute_omega(uint64_t diameter_bound, double eps, double delta, double c) {
+    if (!(eps > 0.0 && eps < 1.0)) invalid("epsilon must lie in (0,1)");
+    if (!(delta > 0.0 && delta < 1.0)) invalid("delta must lie in (0,1)");
+    const uint64_t vd = diameter_bound + 1;
+    const uint64_t arg = vd > 4 ? vd - 2 : 2;
+    const double log2_floor = static_cast<double>(63 - __builtin_clzll(arg));
+    const double value = (c / (eps * eps)) * (log2_floor + 1.0 + std::log(1.0 / delta));
+    return static_cast<uint64_t>(std::ceil(value));
+}
+
+double f_kernel(double b, double log_inv, double omega, double tau) {
+    const double t = 1.0 / 3.0 - omega / tau;
+    return (log_inv / tau) * (t + std::sqrt(t * t + 2.0 * b * omega / log_inv));
+}
+
+double g_kernel(double b, double log_inv, double omega, double tau) {
+    const double t = 1.0 / 3.0 + omega / tau;
+    return (log_inv / tau) * (t + std::sqrt(t * t + 2.0 * b * omega / log_inv));
+}
+
+bool converged_at_max(uint64_t max_count, uint64_t tau, uint64_t omega, double eps, double log_inv) {
+    const double b = static_cast<double>(max_count) / static_cast<double>(tau);
+    if (f_kernel(b, log_inv, static_cast<double>(omega), static_cast<double>(tau)) > eps) return false;
+    if (g_kernel(b, log_inv, static_cast<double>(omega), static_cast<double>(tau)) > eps) return false;
+    return true;
+}
+
+namespace {
+
+constexpr uint32_t kNoStop = 0xFFFFFFFFu;
+
+struct RuleParams {
+    uint64_t omega;
+    double omega_d;
+    double log_inv;
+    double eps;
+};
+
+// kadabra.hpp:59-67 + 148-151 at the maximum count, IEEE _rn ops only.
+__device__ bool rule_passes(uint64_t max_count, uint64_t tau, const RuleParams& r) {
+    if (tau >= r.omega) return true;
+    const double tau_d = __ull2double_rn(tau);
+    const double b = __ddiv_rn(__ull2double_rn(max_count), tau_d);
+    const double two_b_w_l = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, b), r.omega_d), r.log_inv);
+    const double scale = __ddiv_rn(r.log_inv, tau_d);
+    const double w_t = __ddiv_rn(r.omega_d, tau_d);
+    const double tf = __dsub_rn(1.0 / 3.0, w_t);
+    const double f = __dmul_rn(scale, __dadd_rn(tf, __dsqrt_rn(__dadd_rn(__dmul_rn(tf, tf), two_b_w_l))));
+    if (f > r.eps) return false;
+    const double tg = __dadd_rn(1.0 / 3.0, w_t);
+    const double g = __dmul_rn(scale, __dadd_rn(tg, __dsqrt_rn(__dadd_rn(__dmul_rn(tg, tg), two_b_w_l))));
+    return !(g > r.eps);
+}
+
+// K4a: value of each sorted event = count of v after its frame; per-frame max
+__global__ void k_event_values(const unsigned long long* __restrict__ sorted, uint64_t count,
+                               const uint32_t* __restrict__ total, uint32_t* frame_max) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long key = sorted[i];
+        if (key == ~0ull) continue;
+        const unsigned long long target = key & 0xFFFFFFFF00000000ull;
+        uint64_t lo = 0, hi = i;  // first index of this vertex's run
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (sorted[mid] < target) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t v = static_cast<uint32_t>(key >> 32);
+        const uint32_t value = total[v] + static_cast<uint32_t>(i - lo) + 1u;
+        atomicMax(frame_max + static_cast<uint32_t>(key), value);
+    }
+}
+
+// K4b: first frame of the batch at which the rule holds (or the cap frame)
+__global__ void k_find_stop(const uint32_t* __restrict__ run_max, uint32_t frames,
+                            const uint32_t* base_max, uint64_t frames_before, uint64_t spf,
+                            RuleParams r, uint32_t* stop) {
+    const uint32_t bm = *base_max;
+    for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < frames; f += gridDim.x * blockDim.x) {
+        const uint64_t tau = (frames_before + f + 1) * spf;
+        if (rule_passes(max(run_max[f], bm), tau, r)) atomicMin(stop, f);
+    }
+}
+
+// K4c: fold the events of frames <= limit into the running counts
+__global__ void k_apply(const unsigned long long* __restrict__ events, uint64_t count, uint32_t limit,
+                        uint32_t* total) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long key = events[i];
+        if (key == ~0ull) continue;
+        if (static_cast<uint32_t>(key) <= limit) atomicAdd(total + (key >> 32), 1u);
+    }
+}
+
+__global__ void k_update_base(const uint32_t* run_max, uint32_t limit, uint32_t* base_max) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *base_max = max(*base_max, run_max[limit]);
+}
+
+struct MaxOp {
+    __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+// K3: total += epoch; epoch = 0; max over vertices
+__global__ void k_fold_epoch(uint32_t* __restrict__ total, uint32_t* __restrict__ epoch, uint32_t n,
+                             uint32_t* max_out) {
+    uint32_t local = 0;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t t = total[v] + epoch[v];
+        total[v] = t;
+        epoch[v] = 0;
+        local = max(local, t);
+    }
+    using BlockReduce = cub::BlockReduce<uint32_t, 256>;
+    __shared__ typename BlockReduce::TempStorage tmp;
+    const uint32_t bmax = BlockReduce(tmp).Reduce(local, MaxOp());
+    if (threadIdx.x == 0) atomicMax(max_out, bmax);
+}
+
+__global__ void k_epoch_rule(uint32_t* max_in, uint64_t tau, RuleParams r, uint32_t* flag) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *flag = rule_passes(*max_in, tau, r) ? 1u : 0u;
+        *max_in = 0;
+    }
+}
+
+unsigned grid_for(uint64_t work, int device) {
+    const uint64_t want = (work + 255) / 256;
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, num_sms(device) * 8ull)));
+}
+
+struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double seconds() const {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
+    const uint32_t n = ctx.graph.n;
+    if (ctx.arena && ctx.arena->level_cap >= level_cap) return;
+    ctx.arena.reset();
+    ADSB_CUDA(cudaSetDevice(ctx.device));
+    const int sms = num_sms(ctx.device);
+    const int per_sm = std::max(sampler_warps_per_sm(true), 8);
+    size_t free_b = 0, total_b = 0;
+    ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t per_slot = static_cast<uint64_t>(n) * (16 + 4 + 8) + static_cast<uint64_t>(level_cap) * 4;
+    const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
+    uint64_t slots = static_cast<uint64_t>(sms) * per_sm;
+    slots = std::min<uint64_t>(slots, budget / std::max<uint64_t>(per_slot, 1));
+    slots = slots / 8 * 8;
+    if (slots < 8)
+        fail(ADSB_ERR_CUDA, "not enough device memory for the sampler scratch (" +
+                                std::to_string(per_slot >> 20) + " MiB per team)");
+    auto a = std::make_unique<SamplerArena>();
+    a->slots = static_cast<uint32_t>(slots);
+    a->n = n;
+    a->level_cap = level_cap;
+    a->state.alloc(slots * n * 2);
+    a->queue.alloc(slots * n);
+    a->qrange.alloc(slots * n);
+    a->tlev.alloc(slots * level_cap);
+    a->slot_tag.alloc(slots);
+    ADSB_CUDA(cudaMemsetAsync(a->state.ptr, 0, a->state.bytes(), ctx.stream));
+    ADSB_CUDA(cudaMemsetAsync(a->slot_tag.ptr, 0, a->slot_tag.bytes(), ctx.stream));
+    ADSB_CUDA(cudaStreamSynchronize(ctx.stream));
+    ctx.arena = std::move(a);
+}
+
+SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
+    SamplerArena& a = *ctx.arena;
+    SamplerParams p{};
+    p.off = ctx.graph.offsets.ptr;
+    p.nbrs = ctx.graph.nbrs.ptr;
+    p.label = ctx.labels.ptr;
+    p.n = ctx.graph.n;
+    p.slots = a.slots;
+    p.level_cap = a.level_cap;
+    p.rank = 0;
+    p.world = 1;
+    p.seed = seed;
+    p.spf = spf;
+    p.state = a.state.ptr;
+    p.queue = a.queue.ptr;
+    p.qrange = a.qrange.ptr;
+    p.tlev = a.tlev.ptr;
+    p.slot_tag = a.slot_tag.ptr;
+    return p;
+}
+
+struct Launches {
+    uint64_t count = 0;
+};
+
+// One deterministic batch through the sampler; grows the event buffer until it fits.
+uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, DevBuf<unsigned long long>& events,
+                       DevBuf<unsigned long long>& scal, Launches& L, cudaEvent_t e0, cudaEvent_t e1,
+                       double& sampler_ms) {
+    for (;;) {
+        ADSB_CUDA(cudaMemsetAsync(scal.ptr, 0, 2 * sizeof(unsigned long long), ctx.stream));
+        p.ticket = scal.ptr;
+        p.ev_cursor = scal.ptr + 1;
+        p.events = events.ptr;
+        p.ev_cap = events.count;
+        ADSB_CUDA(cudaEventRecord(e0, ctx.stream));
+        launch_sampler(true, p, ctx.stream);
+        ADSB_CUDA(cudaEventRecord(e1, ctx.stream));
+        L.count++;
+        unsigned long long used = 0;
+        ADSB_CUDA(cudaMemcpyAsync(&used, scal.ptr + 1, sizeof(used), cudaMemcpyDeviceToHost, ctx.stream));
+        ADSB_CUDA(cudaStreamSynchronize(ctx.stream));
+        float ms = 0;
+        ADSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        sampler_ms += ms;
+        if (used <= events.count) return used;
+        events.alloc(used + used / 4 + 1024);  // deterministic: rerun the same batch
+    }
+}
+
+}  // namespace
+
+EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const EngineOptions& opt) {
+    EngineOutput out;
+    const uint32_t n = ctx.graph.n;
+    if (n == 0) invalid("graph has no vertices");
+    if (!(delta > 0.0 && delta < 1.0)) invalid("delta must lie in (0,1)");
+    if (!(eps > 0.0 && eps < 1.0)) invalid("epsilon must lie in (0,1)");
+    ADSB_CUDA(cudaSetDevice(ctx.device));
+    if (n == 1) {  // kadabra.hpp:314-317
+        out.counts.assign(1, 0);
+        return out;
+    }
+    const int world = opt.comm ? opt.comm->nranks : 1;
+    const int rank = opt.comm ? opt.comm->rank : 0;
+
+    // ---- preprocessing (kadabra.hpp:319-325): components, D_ub, omega, deltas
+    Timer pre;
+    ctx.labels_ready = false;  // recomputed per call, as the reference does
+    out.num_components = device_components(ctx);
+    out.diameter_bound = device_diameter_bound(ctx);
+    out.omega = compute_omega(out.diameter_bound, eps, delta, opt.c);
+    const double delta_v = delta / (2.0 * static_cast<double>(n));  // kadabra.hpp:34
+    const double log_inv = std::log(1.0 / delta_v);                 // kadabra.hpp:123
+    const uint32_t level_cap = static_cast<uint32_t>(std::min<uint64_t>(out.diameter_bound + 3, n + 2));
+    ensure_arena(ctx, level_cap);
+    out.preprocess_seconds = pre.seconds();
+
+    Timer ads;
+    const RuleParams rule{out.omega, static_cast<double>(out.omega), log_inv, eps};
+    cudaStream_t s1 = ctx.stream, s2 = ctx.stream2;
+    DevBuf<uint32_t> total(n);
+    DevBuf<unsigned long long> stats(kStatCount);
+    DevBuf<unsigned long long> scal(4);
+    ADSB_CUDA(cudaMemsetAsync(total.ptr, 0, total.bytes(), s1));
+    ADSB_CUDA(cudaMemsetAsync(stats.ptr, 0, stats.bytes(), s1));
+    cudaEvent_t e0, e1;
+    ADSB_CUDA(cudaEventCreate(&e0));
+    ADSB_CUDA(cudaEventCreate(&e1));
+    Launches L;
+    const uint64_t team_slots = ctx.arena->slots;
+
+    if (opt.deterministic) {
+        const uint64_t spf = opt.spf;
+        uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
+        if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
+        frame_limit = std::max<uint64_t>(frame_limit, 1);
+        DevBuf<uint32_t> base_max(1), stop_idx(1);
+        ADSB_CUDA(cudaMemsetAsync(base_max.ptr, 0, sizeof(uint32_t), s1));
+        DevBuf<unsigned long long> events(1 << 20), sorted, gathered;
+        DevBuf<uint32_t> frame_max, run_max;
+        DevBuf<uint8_t> temp;
+        uint64_t done = 0;  // frames folded so far
+        uint64_t sampled_frames = 0;
+        bool stopped = false;
+        uint32_t stop_local = kNoStop;
+        while (!stopped) {
+            uint64_t F = std::max<uint64_t>(2 * team_slots * world, done);
+            F = std::min<uint64_t>(F, frame_limit - done);
+            F = std::min<uint64_t>(F, 1ull << 30);
+            SamplerParams p = base_params(ctx, opt.seed, spf);
+            p.first = done;
+            p.rank = static_cast<uint32_t>(rank);
+            p.world = static_cast<uint32_t>(world);
+            p.num_items = (F > static_cast<uint64_t>(rank)) ? (F - rank + world - 1) / world : 0;
+            p.stats = stats.ptr;
+            uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, out.sampler_ms);
+            sampled_frames += F;
+            unsigned long long* ev = events.ptr;
+            uint64_t count = E;
+            if (world > 1 || opt.comm) {
+                // gather every rank's events so each rank runs the identical cutoff
+                DevBuf<unsigned long long> dmax(1);
+                unsigned long long mine = E;
+                ADSB_CUDA(cudaMemcpyAsync(dmax.ptr, &mine, sizeof(mine), cudaMemcpyHostToDevice, s1));
+                ADSB_NCCL(ncclAllReduce(dmax.ptr, dmax.ptr, 1, ncclUint64, ncclMax, opt.comm->comm, s1));
+                unsigned long long emax = 0;
+                ADSB_CUDA(cudaMemcpyAsync(&emax, dmax.ptr, sizeof(emax), cudaMemcpyDeviceToHost, s1));
+                ADSB_CUDA(cudaStreamSynchronize(s1));
+                if (events.count < emax) {
+                    DevBuf<unsigned long long> grown(emax);
+                    ADSB_CUDA(cudaMemcpyAsync(grown.ptr, events.ptr, E * sizeof(unsigned long long),
+                                              cudaMemcpyDeviceToDevice, s1));
+                    events = std::move(grown);
+                }
+                if (emax > E)
+                    ADSB_CUDA(cudaMemsetAsync(events.ptr + E, 0xFF, (emax - E) * sizeof(unsigned long long), s1));
+                if (gathered.count < emax * world) gathered.alloc(emax * world);
+                ADSB_NCCL(ncclAllGather(events.ptr, gathered.ptr, emax, ncclUint64, opt.comm->comm, s1));
+                ev = gathered.ptr;
+                count = emax * world;
+            }
+            // K4: ordered cutoff over the batch
+            if (sorted.count < count) sorted.alloc(count + count / 4 + 1);
+            if (frame_max.count < F) {
+                frame_max.alloc(F);
+                run_max.alloc(F);
+            }
+            int end_bit = 64;
+            if (world == 1 && !opt.comm) {
+                int vbits = 1;
+                while (vbits < 32 && (1ull << vbits) < n) ++vbits;
+                end_bit = 32 + vbits;
+            }
+            size_t tb = 0;
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, ev, sorted.ptr, count, 0, end_bit, s1));
+            size_t tb2 = 0;
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, frame_max.ptr, run_max.ptr, MaxOp(),
+                                                     static_cast<int64_t>(F), s1));
+            tb = std::max(tb, tb2);
+            if (temp.count < tb) temp.alloc(tb);
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(temp.ptr, tb, ev, sorted.ptr, count, 0, end_bit, s1));
+            ADSB_CUDA(cudaMemsetAsync(frame_max.ptr, 0, F * sizeof(uint32_t), s1));
+            k_event_values<<<grid_for(count, ctx.device), 256, 0, s1>>>(sorted.ptr, count, total.ptr, frame_max.ptr);
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp.ptr, tb, frame_max.ptr, run_max.ptr, MaxOp(),
+                                                     static_cast<int64_t>(F), s1));
+            ADSB_CUDA(cudaMemsetAsync(stop_idx.ptr, 0xFF, sizeof(uint32_t), s1));
+            k_find_stop<<<grid_for(F, ctx.device), 256, 0, s1>>>(run_max.ptr, static_cast<uint32_t>(F),
+                                                                 base_max.ptr, done, spf, rule, stop_idx.ptr);
+            uint32_t stop_host = kNoStop;
+            ADSB_CUDA(cudaMemcpyAsync(&stop_host, stop_idx.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
+            ADSB_CUDA(cudaStreamSynchronize(s1));
+            L.count += 3;
+            uint32_t limit = static_cast<uint32_t>(F - 1);
+            if (stop_host != kNoStop) {
+                limit = stop_host;
+                stopped = true;
+                stop_local = stop_host;
+            } else if (done + F >= frame_limit) {
+                stopped = true;  // max_cycles cap
+                stop_local = limit;
+                out.reason = ADSB_REASON_CAPPED;
+            }
+            k_apply<<<grid_for(count, ctx.device), 256, 0, s1>>>(ev, count, limit, total.ptr);
+            k_update_base<<<1, 32, 0, s1>>>(run_max.ptr, limit, base_max.ptr);
+            L.count += 2;
+            if (!stopped) done += F;
+            else done += static_cast<uint64_t>(stop_local) + 1;
+        }
+        out.total_samples = sampled_frames * spf;
+        out.check_cycles = done;
+        out.tau = done * spf;
+        out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
+    } else {
+        // ---- cumulative epoch pipeline
+        uint64_t B = opt.epoch_samples;
+        if (B == 0) {
+            B = std::max<uint64_t>(4 * team_slots * world, 1024);
+            B = std::min<uint64_t>(B, std::max<uint64_t>(out.omega / 4, 1024));
+        }
+        uint64_t max_epochs = (out.omega + B - 1) / B;
+        if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
+        max_epochs = std::max<uint64_t>(max_epochs, 1);
+        DevBuf<uint32_t> cnt(2ull * n), dmax(2), flag_dev(2);
+        DevBuf<unsigned long long> tickets(2);
+        PinnedBuf<uint32_t> flag_host(2);
+        ADSB_CUDA(cudaMemsetAsync(cnt.ptr, 0, cnt.bytes(), s1));
+        ADSB_CUDA(cudaMemsetAsync(dmax.ptr, 0, dmax.bytes(), s1));
+        ADSB_CUDA(cudaStreamSynchronize(s1));
+        cudaEvent_t samp[2], chk[2];
+        for (int i = 0; i < 2; ++i) {
+            ADSB_CUDA(cudaEventCreateWithFlags(&samp[i], cudaEventDisableTiming));
+            ADSB_CUDA(cudaEventCreateWithFlags(&chk[i], cudaEventDisableTiming));
+        }
+        const uint64_t share = (B > static_cast<uint64_t>(rank)) ? (B - rank + world - 1) / world : 0;
+        uint64_t launched = 0;
+        auto enqueue_sampler = [&](uint64_t e) {
+            const int k = static_cast<int>(e & 1);
+            if (e >= 2) ADSB_CUDA(cudaStreamWaitEvent(s1, chk[k], 0));
+            SamplerParams p = base_params(ctx, opt.seed, 1);
+            p.first = e * B;
+            p.rank = static_cast<uint32_t>(rank);
+            p.world = static_cast<uint32_t>(world);
+            p.num_items = share;
+            p.ticket = tickets.ptr + k;
+            p.counts = cnt.ptr + static_cast<size_t>(k) * n;
+            p.stats = stats.ptr;
+            ADSB_CUDA(cudaMemsetAsync(tickets.ptr + k, 0, sizeof(unsigned long long), s1));
+            launch_sampler(false, p, s1);
+            ADSB_CUDA(cudaEventRecord(samp[k], s1));
+            L.count++;
+            launched++;
+        };
+        auto enqueue_check = [&](uint64_t e) {
+            const int k = static_cast<int>(e & 1);
+            ADSB_CUDA(cudaStreamWaitEvent(s2, samp[k], 0));
+            uint32_t* ec = cnt.ptr + static_cast<size_t>(k) * n;
+            if (opt.comm) ADSB_NCCL(ncclAllReduce(ec, ec, n, ncclUint32, ncclSum, opt.comm->comm, s2));
+            k_fold_epoch<<<grid_for(n, ctx.device), 256, 0, s2>>>(total.ptr, ec, n, dmax.ptr + k);
+            k_epoch_rule<<<1, 32, 0, s2>>>(dmax.ptr + k, (e + 1) * B, rule, flag_dev.ptr + k);
+            ADSB_CUDA(cudaMemcpyAsync(flag_host.ptr + k, flag_dev.ptr + k, sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, s2));
+            ADSB_CUDA(cudaEventRecord(chk[k], s2));
+            L.count += 2;
+        };
+        cudaEvent_t t_begin, t_end;
+        ADSB_CUDA(cudaEventCreate(&t_begin));
+        ADSB_CUDA(cudaEventCreate(&t_end));
+        ADSB_CUDA(cudaEventRecord(t_begin, s1));
+        enqueue_sampler(0);
+        enqueue_check(0);
+        if (max_epochs > 1) enqueue_sampler(1);
+        uint64_t e = 0;
+        for (;; ++e) {
+            const int k = static_cast<int>(e & 1);
+            ADSB_CUDA(cudaEventSynchronize(chk[k]));
+            const bool pass = flag_host.ptr[k] != 0;
+            if (pass || e + 1 >= max_epochs) {
+                if (!pass) out.reason = ADSB_REASON_CAPPED;
+                break;
+            }
+            enqueue_check(e + 1);
+            if (e + 2 < max_epochs) enqueue_sampler(e + 2);
+        }
+        ADSB_CUDA(cudaEventRecord(t_end, s1));
+        ADSB_CUDA(cudaStreamSynchronize(s1));
+        ADSB_CUDA(cudaStreamSynchronize(s2));
+        float ms = 0;
+        ADSB_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
+        out.sampler_ms = ms;  // sampling stream busy span (epochs back to back)
+        out.tau = (e + 1) * B;
+        out.check_cycles = e + 1;
+        out.stop_epoch = e + 1;
+        out.total_samples = launched * B;
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(samp[i]);
+            cudaEventDestroy(chk[i]);
+        }
+        cudaEventDestroy(t_begin);
+        cudaEventDestroy(t_end);
+    }
+
+    // ---- results
+    std::vector<uint32_t> host32(n);
+    ADSB_CUDA(cudaMemcpyAsync(host32.data(), total.ptr, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
+    unsigned long long st_host[kStatCount];
+    ADSB_CUDA(cudaMemcpyAsync(st_host, stats.ptr, sizeof(st_host), cudaMemcpyDeviceToHost, s1));
+    ADSB_CUDA(cudaStreamSynchronize(s1));
+    ADSB_CUDA(cudaGetLastError());
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (st_host[kStatErrors] != 0)
+        fail(ADSB_ERR_LOGIC, "sampler reported " + std::to_string(st_host[kStatErrors]) +
+                                 " inconsistent traversals (all predecessor counts wrapped to 0?)");
+    out.counts.assign(host32.begin(), host32.end());
+    out.edges_scanned = st_host[kStatEdges];
+    out.vertices_expanded = st_host[kStatVertices];
+    out.kernel_launches = L.count;
+    // kadabra.hpp:339-343
+    if (out.reason != ADSB_REASON_CAPPED) {
+        out.reason = ADSB_REASON_OMEGA_REACHED;
+        uint64_t mx = 0;
+        for (uint32_t v : host32) mx = std::max<uint64_t>(mx, v);
+        if (out.tau >= 1 && converged_at_max(mx, out.tau, out.omega, eps, log_inv))
+            out.reason = ADSB_REASON_EPS_CONVERGED;
+    }
+    out.ads_seconds = ads.seconds();
+    return out;
+}
+
+void sample_frames(DeviceContext& ctx, uint64_t seed, uint64_t spf, uint64_t first, uint64_t count,
+                   uint64_t* frame_offsets, uint32_t* incs, uint64_t cap) {
+    if (spf < 1) invalid("samples per frame must be >= 1");
+    if (count == 0) {
+        frame_offsets[0] = 0;
+        return;
+    }
+    if (count >= (1ull << 32)) invalid("too many frames");
+    ADSB_CUDA(cudaSetDevice(ctx.device));
+    device_components(ctx);
+    const uint64_t dub = device_diameter_bound(ctx);
+    ensure_arena(ctx, static_cast<uint32_t>(std::min<uint64_t>(dub + 3, ctx.graph.n + 2)));
+    DevBuf<unsigned long long> events(1 << 16), scal(4), stats(kStatCount);
+    ADSB_CUDA(cudaMemsetAsync(stats.ptr, 0, stats.bytes(), ctx.stream));
+    SamplerParams p = base_params(ctx, seed, spf);
+    p.first = first;
+    p.num_items = count;
+    p.stats = stats.ptr;
+    cudaEvent_t e0, e1;
+    ADSB_CUDA(cudaEventCreate(&e0));
+    ADSB_CUDA(cudaEventCreate(&e1));
+    Launches L;
+    double ms = 0;
+    const uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, ms);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::vector<unsigned long long> host(E);
+    unsigned long long st_host[kStatCount];
+    ADSB_CUDA(cudaMemcpy(host.data(), events.ptr, E * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    ADSB_CUDA(cudaMemcpy(st_host, stats.ptr, sizeof(st_host), cudaMemcpyDeviceToHost));
+    if (st_host[kStatErrors] != 0) fail(ADSB_ERR_LOGIC, "sampler reported inconsistent traversals");
+    // Events of one frame were reserved in sample order, each sample's in t->s
+    // order, so a stable partition by frame restores the reference's layout.
+    std::vector<uint64_t> per(count + 1, 0);
+    for (auto k : host) per[static_cast<uint32_t>(k) + 1]++;
+    for (uint64_t f = 0; f < count; ++f) per[f + 1] += per[f];
+    std::memcpy(frame_offsets, per.data(), (count + 1) * sizeof(uint64_t));
+    std::vector<uint64_t> cur(per.begin(), per.end() - 1);
+    for (uint64_t i = 0; i < E; ++i) {
+        const uint64_t slot = cur[static_cast<uint32_t>(host[i])]++;
+        if (slot < cap) incs[slot] = static_cast<uint32_t>(host[i] >> 32);
+    }
+}
+
+}  // namespace adsb

@@ -1,0 +1,420 @@
+// graph_host.cpp — edge-list ingestion and CSR construction (host).
+//
+// Semantics follow the reference exactly (paths relative to
+// /root/reference/proj/include/adsamp/):
+//   * graph.hpp:93-131  parse_edge_list — line-based; a line whose first char
+//     outside " \t\r" is '%' or '#' is a comment; otherwise two ids read as
+//     `istream >> uint64_t` would (skip whitespace, optional sign, decimal
+//     digits, overflow fails), then no trailing token, then ids <= 2^32-1.
+//     Dense ids follow first appearance (a then b, line by line), self-loop
+//     lines included.
+//   * graph.hpp:35-58   from_edges — self-loops dropped, both directions,
+//     sorted, deduplicated, so every adjacency list is ascending.
+// The CSR build is parallel (counting scatter + per-list sort/unique) rather
+// than the reference's single global sort; the result is identical.
+#include "graph_host.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <numeric>
+#include <set>
+#include <thread>
+#include <unordered_map>
+
+#include "common.hpp"
+#include "rng.hpp"
+
+namespace adsb {
+
+unsigned host_threads() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw == 0 ? 1 : std::min(hw, 64u);
+}
+
+template <class F>
+static void parallel_for(uint64_t count, F&& body) {
+    const unsigned T = host_threads();
+    if (count < 65536 || T == 1) {
+        body(0, count);
+        return;
+    }
+    std::vector<std::thread> th;
+    const uint64_t chunk = (count + T - 1) / T;
+    for (unsigned t = 0; t < T; ++t) {
+        const uint64_t b = t * chunk, e = std::min(count, b + chunk);
+        if (b >= e) break;
+        th.emplace_back([&, b, e] { body(b, e); });
+    }
+    for (auto& x : th) x.join();
+}
+
+HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
+    HostGraph g;
+    g.n = n;
+    std::vector<uint64_t> deg(static_cast<size_t>(n) + 1, 0);
+    for (uint64_t i = 0; i < m; ++i) {
+        const uint32_t u = edges[2 * i], v = edges[2 * i + 1];
+        if (u == v) continue;
+        if (u >= n || v >= n) invalid("edge endpoint out of range");
+        deg[u + 1]++;
+        deg[v + 1]++;
+    }
+    for (uint32_t u = 0; u < n; ++u) deg[u + 1] += deg[u];
+    std::vector<uint32_t> raw(deg[n]);
+    {
+        std::vector<uint64_t> cur(deg.begin(), deg.end() - 1);
+        for (uint64_t i = 0; i < m; ++i) {
+            const uint32_t u = edges[2 * i], v = edges[2 * i + 1];
+            if (u == v) continue;
+            raw[cur[u]++] = v;
+            raw[cur[v]++] = u;
+        }
+    }
+    // sort + unique each list in place; record the deduplicated degree
+    std::vector<uint64_t> kept(static_cast<size_t>(n) + 1, 0);
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+        for (uint64_t u = b; u < e; ++u) {
+            uint32_t* first = raw.data() + deg[u];
+            uint32_t* last = raw.data() + deg[u + 1];
+            std::sort(first, last);
+            kept[u + 1] = static_cast<uint64_t>(std::unique(first, last) - first);
+        }
+    });
+    for (uint32_t u = 0; u < n; ++u) kept[u + 1] += kept[u];
+    g.nbrs.resize(kept[n]);
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+        for (uint64_t u = b; u < e; ++u)
+            std::memcpy(g.nbrs.data() + kept[u], raw.data() + deg[u],
+                        (kept[u + 1] - kept[u]) * sizeof(uint32_t));
+    });
+    g.offsets = std::move(kept);
+    g.original_ids.resize(n);
+    std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});
+    return g;
+}
+
+HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs) {
+    if (offsets[0] != 0) invalid("offsets[0] must be 0");
+    for (uint32_t u = 0; u < n; ++u)
+        if (offsets[u + 1] < offsets[u]) invalid("offsets must be non-decreasing");
+    HostGraph g;
+    g.n = n;
+    g.offsets.assign(offsets, offsets + static_cast<size_t>(n) + 1);
+    g.nbrs.assign(nbrs, nbrs + offsets[n]);
+    std::atomic<bool> bad{false};
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+        for (uint64_t u = b; u < e && !bad.load(std::memory_order_relaxed); ++u)
+            for (uint64_t i = g.offsets[u]; i < g.offsets[u + 1]; ++i) {
+                const uint32_t v = g.nbrs[i];
+                if (v >= n || v == u || (i > g.offsets[u] && g.nbrs[i - 1] >= v)) bad = true;
+            }
+    });
+    if (bad) invalid("CSR must have in-range, ascending, duplicate-free, loop-free adjacency");
+    g.original_ids.resize(n);
+    std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});
+    return g;
+}
+
+namespace {
+
+// First-appearance interning (graph.hpp:98-104). Dense small ids go through a
+// direct table; anything else through a hash map.
+struct Interner {
+    std::vector<uint64_t> ids;
+    std::unordered_map<uint64_t, uint32_t> map;
+    std::vector<uint32_t> table;  // id -> dense+1 while ids stay below table.size()
+    static constexpr uint64_t kTableLimit = uint64_t{1} << 27;
+
+    uint32_t operator()(uint64_t id) {
+        if (id < kTableLimit) {
+            if (id >= table.size()) table.resize(std::min<uint64_t>(kTableLimit, std::max<uint64_t>(id + 1, 2 * table.size())), 0);
+            uint32_t& slot = table[id];
+            if (slot == 0) {
+                ids.push_back(id);
+                slot = static_cast<uint32_t>(ids.size());
+            }
+            return slot - 1;
+        }
+        auto [it, inserted] = map.try_emplace(id, static_cast<uint32_t>(ids.size()));
+        if (inserted) ids.push_back(id);
+        return it->second;
+    }
+};
+
+bool is_space(char c) {
+    return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
+}
+
+// `istream >> uint64_t` (libstdc++ num_get): see file header.
+bool get_u64(const char*& p, const char* e, uint64_t& out) {
+    while (p < e && is_space(*p)) ++p;
+    bool neg = false;
+    if (p < e && (*p == '+' || *p == '-')) {
+        neg = *p == '-';
+        ++p;
+    }
+    if (p == e || *p < '0' || *p > '9') return false;
+    uint64_t v = 0;
+    bool overflow = false;
+    while (p < e && *p >= '0' && *p <= '9') {
+        const uint64_t d = static_cast<uint64_t>(*p - '0');
+        if (v > (UINT64_MAX - d) / 10) overflow = true;
+        v = v * 10 + d;
+        ++p;
+    }
+    if (overflow) return false;
+    out = neg ? static_cast<uint64_t>(0 - v) : v;
+    return true;
+}
+
+HostGraph finish(Interner& in, const std::vector<uint32_t>& edges) {
+    if (in.ids.empty()) parse_error("no vertices found in edge list");
+    HostGraph g = graph_from_edges(static_cast<uint32_t>(in.ids.size()), edges.data(), edges.size() / 2);
+    g.original_ids = std::move(in.ids);
+    g.has_original_ids = true;
+    return g;
+}
+
+}  // namespace
+
+HostGraph parse_edge_list_text(const char* text, uint64_t len) {
+    Interner in;
+    std::vector<uint32_t> edges;
+    const char* p = text;
+    const char* end = text + len;
+    uint64_t line_no = 0;
+    while (p < end) {
+        const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
+        const char* le = nl ? nl : end;
+        ++line_no;
+        const char* q = p;
+        while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
+        if (q == le || *q == '%' || *q == '#') {
+            p = nl ? nl + 1 : end;
+            continue;
+        }
+        const char* c = p;
+        uint64_t a = 0, b = 0;
+        if (!get_u64(c, le, a) || !get_u64(c, le, b))
+            parse_error("line " + std::to_string(line_no) + ": expected two vertex ids");
+        while (c < le && is_space(*c)) ++c;
+        if (c < le) {
+            const char* te = c;
+            while (te < le && !is_space(*te)) ++te;
+            parse_error("line " + std::to_string(line_no) + ": trailing token '" + std::string(c, te) + "'");
+        }
+        if (a > 0xFFFFFFFFull || b > 0xFFFFFFFFull)
+            parse_error("line " + std::to_string(line_no) + ": vertex id exceeds 2^32-1");
+        const uint32_t da = in(a);  // interning order fixes the dense numbering
+        const uint32_t db = in(b);
+        edges.push_back(da);
+        edges.push_back(db);
+        p = nl ? nl + 1 : end;
+    }
+    return finish(in, edges);
+}
+
+HostGraph parse_edge_list_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) fail(ADSB_ERR_RUNTIME, "cannot open graph file '" + path + "'");
+    f.seekg(0, std::ios::end);
+    const auto size = static_cast<uint64_t>(f.tellg());
+    f.seekg(0, std::ios::beg);
+    std::string buf(size, '\0');
+    f.read(buf.data(), static_cast<std::streamsize>(size));
+    return parse_edge_list_text(buf.data(), size);
+}
+
+HostGraph graph_from_pairs(const uint64_t* pairs, uint64_t m) {
+    Interner in;
+    std::vector<uint32_t> edges(2 * m);
+    for (uint64_t i = 0; i < m; ++i) {
+        const uint64_t a = pairs[2 * i], b = pairs[2 * i + 1];
+        if (a > 0xFFFFFFFFull || b > 0xFFFFFFFFull)
+            parse_error("line " + std::to_string(i + 1) + ": vertex id exceeds 2^32-1");
+        edges[2 * i] = in(a);
+        edges[2 * i + 1] = in(b);
+    }
+    return finish(in, edges);
+}
+
+// graph.hpp:140-144
+std::string serialize_edge_list(const HostGraph& g) {
+    std::string out;
+    char line[32];
+    for (uint32_t u = 0; u < g.n; ++u)
+        for (uint64_t i = g.offsets[u]; i < g.offsets[u + 1]; ++i)
+            if (u < g.nbrs[i]) {
+                const int k = std::snprintf(line, sizeof(line), "%u %u\n", u, g.nbrs[i]);
+                out.append(line, static_cast<size_t>(k));
+            }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// Generators
+// ---------------------------------------------------------------------------
+
+// G(n, m) exactly as the reference acceptance suite builds it
+// (tests/acceptance.cpp:34-46): distinct unordered pairs drawn with
+// next_below(n) until m are collected, emitted in sorted (u < v) order.
+std::vector<uint64_t> gen_gnm(uint32_t n, uint64_t m, uint64_t seed) {
+    if (n < 2) invalid("G(n,m) needs n >= 2");
+    if (m > static_cast<uint64_t>(n) * (n - 1) / 2) invalid("G(n,m): m exceeds n(n-1)/2");
+    SplitMix64 rng(seed);
+    std::set<std::pair<uint32_t, uint32_t>> edges;
+    while (edges.size() < m) {
+        auto u = static_cast<uint32_t>(rng.next_below(n));
+        auto v = static_cast<uint32_t>(rng.next_below(n));
+        if (u == v) continue;
+        if (u > v) std::swap(u, v);
+        edges.insert({u, v});
+    }
+    std::vector<uint64_t> out;
+    out.reserve(2 * m);
+    for (auto [u, v] : edges) {
+        out.push_back(u);
+        out.push_back(v);
+    }
+    return out;
+}
+
+// R-MAT: edge i draws `scale` quadrant choices from stream reseed(seed, i),
+// each from a 53-bit uniform, most significant bit first. Self-loops dropped,
+// duplicates kept (from_edges collapses them).
+std::vector<uint64_t> gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                               uint64_t seed) {
+    if (scale < 1 || scale > 31) invalid("R-MAT scale must lie in [1, 31]");
+    if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) invalid("R-MAT probabilities invalid");
+    const uint64_t m = static_cast<uint64_t>(edge_factor) << scale;
+    std::vector<uint64_t> raw(2 * m);
+    std::vector<uint8_t> loop(m);
+    const double ab = a + b, abc = a + b + c;
+    parallel_for(m, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t i = lo; i < hi; ++i) {
+            SplitMix64 rng(reseed(seed, i));
+            uint64_t u = 0, v = 0;
+            for (uint32_t bit = 0; bit < scale; ++bit) {
+                const double r = static_cast<double>(rng.next() >> 11) * 0x1.0p-53;
+                const uint64_t bu = r >= ab ? 1 : 0;
+                const uint64_t bv = (r >= a && r < ab) || r >= abc ? 1 : 0;
+                u = (u << 1) | bu;
+                v = (v << 1) | bv;
+            }
+            raw[2 * i] = u;
+            raw[2 * i + 1] = v;
+            loop[i] = u == v;
+        }
+    });
+    std::vector<uint64_t> out;
+    out.reserve(2 * m);
+    for (uint64_t i = 0; i < m; ++i)
+        if (!loop[i]) {
+            out.push_back(raw[2 * i]);
+            out.push_back(raw[2 * i + 1]);
+        }
+    return out;
+}
+
+// Barabasi-Albert: K_{m+1} on 0..m (pairs i<j in lexicographic order), then
+// each new vertex v picks m distinct targets uniformly from the endpoint list
+// (degree-proportional), emitting (v, target) in pick order.
+std::vector<uint64_t> gen_ba(uint32_t n, uint32_t m_per, uint64_t seed) {
+    if (m_per < 1 || n <= m_per) invalid("BA needs 1 <= m < n");
+    SplitMix64 rng(seed);
+    std::vector<uint64_t> out;
+    std::vector<uint32_t> endpoints;
+    const uint64_t total = static_cast<uint64_t>(m_per) * (m_per + 1) / 2 +
+                           static_cast<uint64_t>(n - m_per - 1) * m_per;
+    out.reserve(2 * total);
+    endpoints.reserve(2 * total);
+    for (uint32_t i = 0; i <= m_per; ++i)
+        for (uint32_t j = i + 1; j <= m_per; ++j) {
+            out.push_back(i);
+            out.push_back(j);
+            endpoints.push_back(i);
+            endpoints.push_back(j);
+        }
+    std::vector<uint32_t> picked(m_per);
+    for (uint32_t v = m_per + 1; v < n; ++v) {
+        uint32_t k = 0;
+        while (k < m_per) {
+            const uint32_t t = endpoints[rng.next_below(endpoints.size())];
+            bool dup = false;
+            for (uint32_t j = 0; j < k; ++j) dup |= picked[j] == t;
+            if (!dup) picked[k++] = t;
+        }
+        for (uint32_t j = 0; j < m_per; ++j) {
+            out.push_back(v);
+            out.push_back(picked[j]);
+            endpoints.push_back(v);
+            endpoints.push_back(picked[j]);
+        }
+    }
+    return out;
+}
+
+// width x height 4-neighbour lattice, vertex r*width+c; for each vertex in
+// row-major order its right then its down edge, each dropped when
+// next() < p_drop * 2^64 (threshold as tests/test_util.hpp:86).
+std::vector<uint64_t> gen_grid(uint32_t width, uint32_t height, double p_drop, uint64_t seed) {
+    if (width < 1 || height < 1) invalid("grid needs positive dimensions");
+    if (!(p_drop >= 0.0 && p_drop < 1.0)) invalid("grid drop probability must lie in [0,1)");
+    SplitMix64 rng(seed);
+    const auto threshold = static_cast<uint64_t>(p_drop * 18446744073709551616.0);
+    std::vector<uint64_t> out;
+    out.reserve(4ull * width * height);
+    for (uint32_t r = 0; r < height; ++r)
+        for (uint32_t c = 0; c < width; ++c) {
+            const uint64_t u = static_cast<uint64_t>(r) * width + c;
+            if (c + 1 < width && rng.next() >= threshold) {
+                out.push_back(u);
+                out.push_back(u + 1);
+            }
+            if (r + 1 < height && rng.next() >= threshold) {
+                out.push_back(u);
+                out.push_back(u + width);
+            }
+        }
+    return out;
+}
+
+std::vector<uint64_t> keep_lcc(const std::vector<uint64_t>& pairs) {
+    const uint64_t m = pairs.size() / 2;
+    uint64_t max_id = 0;
+    for (uint64_t x : pairs) max_id = std::max(max_id, x);
+    std::vector<uint32_t> parent(max_id + 1);
+    std::iota(parent.begin(), parent.end(), 0u);
+    auto find = [&](uint32_t x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+    };
+    std::vector<uint8_t> present(max_id + 1, 0);
+    for (uint64_t i = 0; i < m; ++i) {
+        const auto u = static_cast<uint32_t>(pairs[2 * i]), v = static_cast<uint32_t>(pairs[2 * i + 1]);
+        if (u == v) continue;
+        present[u] = present[v] = 1;
+        const uint32_t ru = find(u), rv = find(v);
+        if (ru != rv) parent[std::max(ru, rv)] = std::min(ru, rv);
+    }
+    std::vector<uint32_t> size(max_id + 1, 0);
+    for (uint64_t x = 0; x <= max_id; ++x)
+        if (present[x]) size[find(static_cast<uint32_t>(x))]++;
+    uint32_t best = 0;
+    for (uint64_t x = 0; x <= max_id; ++x)
+        if (size[x] > size[best]) best = static_cast<uint32_t>(x);  // roots are component minima
+    std::vector<uint64_t> out;
+    out.reserve(pairs.size());
+    for (uint64_t i = 0; i < m; ++i) {
+        const auto u = static_cast<uint32_t>(pairs[2 * i]), v = static_cast<uint32_t>(pairs[2 * i + 1]);
+        if (u == v || find(u) != best) continue;
+        out.push_back(u);
+        out.push_back(v);
+    }
+    return out;
+}
+
+}  // namespace adsb

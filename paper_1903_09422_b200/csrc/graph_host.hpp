@@ -1,0 +1,46 @@
+// graph_host.hpp — host-side graph ingestion with the reference's semantics.
+//
+//   parse_edge_list   graph.hpp:93-131  (first-appearance remap, comments, errors)
+//   from_edges        graph.hpp:35-58   (drop self-loops, symmetrise, sort, dedup)
+//
+// The CSR built here is uploaded once per device (graph_device.cuh); all
+// traversal work happens on the GPU.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace adsb {
+
+struct HostGraph {
+    uint32_t n = 0;
+    std::vector<uint64_t> offsets;       // n+1
+    std::vector<uint32_t> nbrs;          // offsets[n], ascending per vertex
+    std::vector<uint64_t> original_ids;  // dense -> id in the input (identity when absent)
+    bool has_original_ids = false;
+
+    uint64_t nnz() const { return nbrs.size(); }
+    uint64_t degree(uint32_t u) const { return offsets[u + 1] - offsets[u]; }
+};
+
+HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m);
+HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs);
+HostGraph parse_edge_list_text(const char* text, uint64_t len);
+HostGraph parse_edge_list_file(const std::string& path);
+HostGraph graph_from_pairs(const uint64_t* pairs, uint64_t m);
+std::string serialize_edge_list(const HostGraph& g);
+
+// Synthetic generators. Output: 2*m original ids.
+std::vector<uint64_t> gen_gnm(uint32_t n, uint64_t m, uint64_t seed);
+std::vector<uint64_t> gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                               uint64_t seed);
+std::vector<uint64_t> gen_ba(uint32_t n, uint32_t m_per, uint64_t seed);
+std::vector<uint64_t> gen_grid(uint32_t width, uint32_t height, double p_drop, uint64_t seed);
+// keep only edges of the largest connected component (ties: the component
+// holding the smallest id); self-loops dropped
+std::vector<uint64_t> keep_lcc(const std::vector<uint64_t>& pairs);
+
+unsigned host_threads();
+
+}  // namespace adsb

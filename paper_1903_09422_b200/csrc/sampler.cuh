@@ -1,0 +1,56 @@
+// sampler.cuh — launch interface of the K1/K2 sampler kernels (sampler.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace adsb {
+
+// Per-vertex state word layout (one u64 "meta" + one u64 sigma per vertex and slot):
+//   bits 63..32  tag   (per-slot sample generation; stale tags mean "unvisited")
+//   bit  31      side  (0: reached from s, 1: reached from t)
+//   bit  30      dag   (t-side vertex on a shortest s-t path)
+//   bits 29..0   distance from the side's root
+constexpr unsigned long long kSideT = 1ull << 31;
+constexpr unsigned long long kDag = 1ull << 30;
+constexpr unsigned long long kDistMask = (1ull << 30) - 1;
+
+enum SamplerStat { kStatEdges = 0, kStatVertices = 1, kStatSamples = 2, kStatErrors = 3, kStatCount = 4 };
+
+struct SamplerParams {
+    // graph (device CSR, u32 offsets) and component labels
+    const uint32_t* off;
+    const uint32_t* nbrs;
+    const uint32_t* label;
+    uint32_t n;
+    uint32_t slots;
+    uint32_t level_cap;
+    uint32_t rank;         // this GPU's rank: items map to positions first + item*world + rank
+    uint32_t world;
+    // work: items [0, num_items) map to stream positions first + item*world + rank
+    uint64_t seed;
+    uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode
+    uint64_t first;
+    uint64_t num_items;
+    unsigned long long* ticket;
+    // slot scratch
+    unsigned long long* state;  // slots * n * 2
+    uint32_t* queue;            // slots * n
+    uint2* qrange;              // slots * n
+    uint32_t* tlev;             // slots * level_cap
+    uint32_t* slot_tag;         // slots
+    // deterministic output: (v << 32) | frame-in-batch
+    unsigned long long* events;
+    unsigned long long* ev_cursor;
+    uint64_t ev_cap;
+    // epoch output: per-vertex counts of this epoch
+    uint32_t* counts;
+    unsigned long long* stats;  // kStatCount
+};
+
+// Resident teams (warps) per SM for the sampler kernel at 256 threads/block.
+int sampler_warps_per_sm(bool deterministic);
+void launch_sampler(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+
+}  // namespace adsb
