@@ -72,9 +72,12 @@ int cmd_run(const std::map<std::string, std::string>& f) {
     const double eps = std::stod(get(f, "--eps", "0.01"));
     const double delta = std::stod(get(f, "--delta", "0.1"));
     const std::uint64_t max_cycles = std::stoull(get(f, "--max-cycles", "0"));
+    const int reps = std::stoi(get(f, "--reps", "1"));
 
     kadabra::BcResult r;
     std::string reason;
+    std::string rep_times;
+    for (int rep = 0; rep < reps; ++rep) {
     if (max_cycles == 0) {
         r = kadabra::estimate_bc(g, eps, delta, cfg);
         reason = kadabra::to_string(r.reason);
@@ -99,6 +102,11 @@ int cmd_run(const std::map<std::string, std::string>& f) {
         r.ads_seconds = std::chrono::duration<double>(t2 - t1).count();
         reason = "capped";
     }
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%s[%.6f, %llu]", rep ? ", " : "", r.ads_seconds,
+                  static_cast<unsigned long long>(r.run.total_samples));
+    rep_times += buf;
+    }
     const auto cpath = get(f, "--counts", "");
     if (!cpath.empty()) {
         std::ofstream out(cpath, std::ios::binary);
@@ -109,14 +117,15 @@ int cmd_run(const std::map<std::string, std::string>& f) {
         "{\"n\": %u, \"m\": %llu, \"variant\": \"%s\", \"threads\": %u, \"spf\": %llu, "
         "\"tau\": %llu, \"check_cycles\": %llu, \"stop_epoch\": %llu, \"omega\": %llu, "
         "\"diameter_bound\": %llu, \"reason\": \"%s\", \"total_samples\": %llu, "
-        "\"preprocess_s\": %.6f, \"ads_s\": %.6f, \"counts_fnv1a\": \"%016llx\"}\n",
+        "\"preprocess_s\": %.6f, \"ads_s\": %.6f, \"counts_fnv1a\": \"%016llx\", "
+        "\"reps\": [%s]}\n",
         g.num_vertices(), static_cast<unsigned long long>(g.num_edges()), to_string(cfg.variant),
         cfg.threads, static_cast<unsigned long long>(cfg.samples_per_frame),
         static_cast<unsigned long long>(r.tau), static_cast<unsigned long long>(r.run.check_cycles),
         static_cast<unsigned long long>(r.run.stop_epoch), static_cast<unsigned long long>(r.omega),
         static_cast<unsigned long long>(r.diameter_bound), reason.c_str(),
         static_cast<unsigned long long>(r.run.total_samples), r.preprocess_seconds, r.ads_seconds,
-        static_cast<unsigned long long>(fnv1a(r.run.data)));
+        static_cast<unsigned long long>(fnv1a(r.run.data)), rep_times.c_str());
     return 0;
 }
 

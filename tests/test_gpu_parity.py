@@ -1,0 +1,145 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact for all integer outputs: sampled paths (and therefore RNG stream
+consumption), per-vertex counts, tau, check_cycles, stop_epoch, D_ub, omega,
+component labels. The oracle itself is pinned to the compiled reference in
+tests/test_oracle.py and tests/golden/.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1903_09422_b200 import adsamp, datasets
+from paper_1903_09422_b200.adsamp import EngineConfig, Variant
+from paper_1903_09422_b200.kadabra import estimate_bc, sample_frames
+
+from conftest import SMALL_GRAPHS
+
+pytestmark = pytest.mark.gpu
+
+
+def both(pairs):
+    return adsamp.graph_from_pairs(pairs), oracle.from_pairs(pairs)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    p = datasets.pairs("c1_er")
+    return both(p)
+
+
+@pytest.fixture(scope="module")
+def grid200():
+    # 200x200 lattice with no drops: sigma exceeds 2^64 for most far pairs (wrap parity)
+    p = datasets.gen_grid(200, 200, 0.0, 3)
+    return both(p)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL_GRAPHS))
+def test_components_and_dub(name):
+    pg, og = both(SMALL_GRAPHS[name]())
+    cc = adsamp.connected_components(pg.graph)
+    lab, comps = oracle.components(og)
+    assert cc.num_components == comps
+    np.testing.assert_array_equal(cc.label, lab)
+    assert adsamp.diameter_upper_bound(pg.graph) == oracle.diameter_upper_bound(og)
+    for s in range(min(og.n, 5)):
+        assert adsamp.eccentricity(pg.graph, s) == oracle.eccentricity(og, s)
+
+
+@pytest.mark.parametrize("name", sorted(SMALL_GRAPHS))
+@pytest.mark.parametrize("spf", [1, 3])
+def test_frames_small(name, spf):
+    pg, og = both(SMALL_GRAPHS[name]())
+    got = sample_frames(pg.graph, 1234, spf, 0, 200)
+    want = oracle.sample_frames(og, 1234, spf, 0, 200)
+    for p, (a, b) in enumerate(zip(got, want)):
+        np.testing.assert_array_equal(a, b, err_msg=f"frame {p}")
+
+
+def test_frames_c1(c1):
+    pg, og = c1
+    got = sample_frames(pg.graph, 42, 1, 0, 4000)
+    want = oracle.sample_frames(og, 42, 1, 0, 4000)
+    assert sum(len(x) for x in want) > 4000
+    for p, (a, b) in enumerate(zip(got, want)):
+        np.testing.assert_array_equal(a, b, err_msg=f"frame {p}")
+    got = sample_frames(pg.graph, 42, 1000, 7, 3)
+    want = oracle.sample_frames(og, 42, 1000, 7, 3)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_frames_sigma_wrap(grid200):
+    pg, og = grid200
+    got = sample_frames(pg.graph, 9, 2, 100, 60)
+    want = oracle.sample_frames(og, 9, 2, 100, 60)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["path3", "star4", "cycle4", "cube", "k23", "er100", "two_components"])
+@pytest.mark.parametrize("spf", [1, 7])
+def test_estimate_det_small(name, spf):
+    pg, og = both(SMALL_GRAPHS[name]())
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=spf, base_seed=5, threads=4)
+    r = estimate_bc(pg.graph, 0.05, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.05, 0.1, spf=spf, seed=5, nominal_threads=4)
+    assert (r.tau, r.run.check_cycles, r.run.stop_epoch, r.omega, r.diameter_bound) == \
+           (o.tau, o.check_cycles, o.stop_epoch, o.omega, o.diameter_bound)
+    assert r.reason.name == o.reason
+    np.testing.assert_array_equal(r.run.data, o.counts)
+    np.testing.assert_array_equal(r.scores, o.scores)
+
+
+@pytest.mark.parametrize("spf", [1, 1000])
+def test_estimate_det_c1(c1, spf):
+    pg, og = c1
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=spf, base_seed=42, threads=8)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.01, 0.1, spf=spf, seed=42, nominal_threads=8)
+    assert (r.tau, r.run.check_cycles, r.run.stop_epoch) == (o.tau, o.check_cycles, o.stop_epoch)
+    assert r.reason.name == o.reason == "eps_converged"
+    np.testing.assert_array_equal(r.run.data, o.counts)
+    assert r.run.total_samples >= r.tau
+
+
+@pytest.mark.parametrize("B", [64, 1000])
+def test_estimate_epoch_small(B):
+    pg, og = both(SMALL_GRAPHS["er100"]())
+    cfg = EngineConfig(variant=Variant.shared, threads=4, base_seed=11, epoch_samples=B)
+    r = estimate_bc(pg.graph, 0.05, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.05, 0.1, mode=oracle.MODE_EPOCH, epoch_samples=B, seed=11)
+    assert (r.tau, r.run.check_cycles) == (o.tau, o.check_cycles)
+    np.testing.assert_array_equal(r.run.data, o.counts)
+
+
+def test_estimate_epoch_c1_within_eps_of_brandes(c1):
+    pg, og = c1
+    exact = oracle.brandes(og)
+    cfg = EngineConfig(variant=Variant.shared, threads=8, base_seed=42, epoch_samples=2048)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.01, 0.1, mode=oracle.MODE_EPOCH, epoch_samples=2048, seed=42)
+    np.testing.assert_array_equal(r.run.data, o.counts)  # epoch semantics are reproducible too
+    assert np.max(np.abs(r.scores - exact)) <= 0.01      # the (eps, delta) guarantee, eps = 0.01
+
+
+def test_capped_runs(c1):
+    pg, og = c1
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=1, base_seed=3, max_cycles=777)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.01, 0.1, spf=1, seed=3, max_frames=777)
+    assert r.tau == o.tau == 777 and r.reason.name == o.reason == "capped"
+    np.testing.assert_array_equal(r.run.data, o.counts)
+
+
+def test_single_vertex_and_errors():
+    pg = adsamp.parse_edge_list("7 7\n")
+    assert pg.graph.num_vertices() == 1
+    r = estimate_bc(pg.graph, 0.05, 0.1, EngineConfig(variant=Variant.indexed))
+    assert r.tau == 0 and list(r.scores) == [0.0]
+    g = adsamp.Graph.from_edges(3, [(0, 1), (1, 2)])
+    with pytest.raises(ValueError):
+        estimate_bc(g, 1.5, 0.1, EngineConfig())
+    with pytest.raises(ValueError):
+        estimate_bc(g, 0.1, 0.0, EngineConfig())
