@@ -91,6 +91,9 @@ typedef struct {
     uint64_t vertices_expanded;  /* frontier vertices expanded (one offsets pair each) */
     uint64_t kernel_launches;    /* adsb kernels launched during the ADS phase */
     double sampler_ms;           /* device time of the sampler kernels (CUDA events) */
+    uint64_t rebuild_edges;      /* of edges_scanned: t-side DAG sigma rebuild */
+    uint64_t backtrack_edges;    /* of edges_scanned: predecessor scans of the backtrack */
+    uint64_t store_fallbacks;    /* samples redone with global-memory state (shared-memory table overflow) */
 } adsb_stats;
 
 void adsb_config_init(adsb_config *cfg); /* reference defaults (engine.hpp:85-96) */

@@ -275,10 +275,10 @@ def ref_available() -> bool:
 
 def ref_run(graph_path, *, eps: float, delta: float, seed: int, variant: str = "indexed", spf: int = 1,
             threads: int = 1, check_interval: int = 1000, max_cycles: int = 0, counts_path=None,
-            timeout: float | None = None) -> dict:
+            timeout: float | None = None, reps: int = 1) -> dict:
     cmd = [str(REF_DRIVER), "run", "--graph", str(graph_path), "--eps", repr(eps), "--delta", repr(delta),
            "--seed", str(seed), "--variant", variant, "--spf", str(spf), "--threads", str(threads),
-           "--check-interval", str(check_interval), "--max-cycles", str(max_cycles)]
+           "--check-interval", str(check_interval), "--max-cycles", str(max_cycles), "--reps", str(reps)]
     if counts_path:
         cmd += ["--counts", str(counts_path)]
     out = subprocess.run(cmd, capture_output=True, text=True, check=True, timeout=timeout)

@@ -77,6 +77,9 @@ class Stats(C.Structure):
         ("vertices_expanded", C.c_uint64),
         ("kernel_launches", C.c_uint64),
         ("sampler_ms", C.c_double),
+        ("rebuild_edges", C.c_uint64),
+        ("backtrack_edges", C.c_uint64),
+        ("store_fallbacks", C.c_uint64),
     ]
 
 

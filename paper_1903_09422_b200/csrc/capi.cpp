@@ -314,6 +314,9 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
             stats->vertices_expanded = r.vertices_expanded;
             stats->kernel_launches = r.kernel_launches;
             stats->sampler_ms = r.sampler_ms;
+            stats->rebuild_edges = r.rebuild_edges;
+            stats->backtrack_edges = r.backtrack_edges;
+            stats->store_fallbacks = r.store_fallbacks;
         }
     });
 }

@@ -83,6 +83,9 @@ struct DeviceGraph {
 // sample team. Each slot holds per-vertex state (16 B), a visit queue with
 // the visited vertices' CSR ranges, and the t-side level boundaries.
 struct SamplerArena {
+    int kind = 1;            // SamplerKind (0 warp teams, 1 block teams)
+    uint32_t hash_cap = 0;   // block teams: shared-memory hash capacity
+    bool use_smem = true;    // block teams: disabled when most samples overflow the table
     uint32_t slots = 0;
     uint32_t n = 0;
     uint32_t level_cap = 0;

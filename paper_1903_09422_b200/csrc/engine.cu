@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "comm.hpp"
@@ -183,18 +184,26 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     ctx.arena.reset();
     ADSB_CUDA(cudaSetDevice(ctx.device));
     const int sms = num_sms(ctx.device);
-    const int per_sm = std::max(sampler_warps_per_sm(true), 8);
+    const SamplerKind kind = sampler_kind();
+    uint32_t hash_cap = 4096;
+    if (const char* e = std::getenv("ADSB_HASH_CAP")) hash_cap = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
+    if (hash_cap < 64 || (hash_cap & (hash_cap - 1))) invalid("ADSB_HASH_CAP must be a power of two >= 64");
+    const int per_sm = kind == SamplerKind::kWarp ? std::max(sampler_warps_per_sm(true), 8)
+                                                  : std::max(sampler_cta_blocks_per_sm(hash_cap), 1);
     size_t free_b = 0, total_b = 0;
     ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t per_slot = static_cast<uint64_t>(n) * (16 + 4 + 8) + static_cast<uint64_t>(level_cap) * 4;
     const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
     uint64_t slots = static_cast<uint64_t>(sms) * per_sm;
     slots = std::min<uint64_t>(slots, budget / std::max<uint64_t>(per_slot, 1));
-    slots = slots / 8 * 8;
-    if (slots < 8)
+    if (kind == SamplerKind::kWarp) slots = slots / 8 * 8;
+    if (slots < (kind == SamplerKind::kWarp ? 8u : 1u))
         fail(ADSB_ERR_CUDA, "not enough device memory for the sampler scratch (" +
                                 std::to_string(per_slot >> 20) + " MiB per team)");
     auto a = std::make_unique<SamplerArena>();
+    a->kind = kind == SamplerKind::kWarp ? 0 : 1;
+    a->hash_cap = hash_cap;
+    a->use_smem = !(std::getenv("ADSB_NO_SMEM"));
     a->slots = static_cast<uint32_t>(slots);
     a->n = n;
     a->level_cap = level_cap;
@@ -227,12 +236,25 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.qrange = a.qrange.ptr;
     p.tlev = a.tlev.ptr;
     p.slot_tag = a.slot_tag.ptr;
+    p.hash_cap = a.hash_cap;
+    p.use_smem = a.use_smem ? 1u : 0u;
     return p;
 }
 
 struct Launches {
     uint64_t count = 0;
 };
+
+// Stop trying the shared-memory table for this graph when most samples
+// overflow it (their balls are too large); results do not depend on the store.
+void adapt_store(DeviceContext& ctx, const unsigned long long* stats, cudaStream_t s) {
+    SamplerArena& a = *ctx.arena;
+    if (a.kind == 0 || !a.use_smem) return;
+    unsigned long long h[kStatCount];
+    ADSB_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+    ADSB_CUDA(cudaStreamSynchronize(s));
+    if (h[kStatSamples] >= 256 && h[kStatFallbacks] * 2 > h[kStatSamples]) a.use_smem = false;
+}
 
 // One deterministic batch through the sampler; grows the event buffer until it fits.
 uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, DevBuf<unsigned long long>& events,
@@ -245,7 +267,7 @@ uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, DevBuf<unsigned long
         p.events = events.ptr;
         p.ev_cap = events.count;
         ADSB_CUDA(cudaEventRecord(e0, ctx.stream));
-        launch_sampler(true, p, ctx.stream);
+        launch_sampler(static_cast<SamplerKind>(ctx.arena->kind == 0 ? 0 : 1), true, p, ctx.stream);
         ADSB_CUDA(cudaEventRecord(e1, ctx.stream));
         L.count++;
         unsigned long long used = 0;
@@ -327,6 +349,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             p.stats = stats.ptr;
             uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, out.sampler_ms);
             sampled_frames += F;
+            adapt_store(ctx, stats.ptr, s1);
             unsigned long long* ev = events.ptr;
             uint64_t count = E;
             if (world > 1 || opt.comm) {
@@ -425,6 +448,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         }
         const uint64_t share = (B > static_cast<uint64_t>(rank)) ? (B - rank + world - 1) / world : 0;
         uint64_t launched = 0;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> launch_ev;
         auto enqueue_sampler = [&](uint64_t e) {
             const int k = static_cast<int>(e & 1);
             if (e >= 2) ADSB_CUDA(cudaStreamWaitEvent(s1, chk[k], 0));
@@ -437,7 +461,13 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             p.counts = cnt.ptr + static_cast<size_t>(k) * n;
             p.stats = stats.ptr;
             ADSB_CUDA(cudaMemsetAsync(tickets.ptr + k, 0, sizeof(unsigned long long), s1));
-            launch_sampler(false, p, s1);
+            cudaEvent_t a, b;
+            ADSB_CUDA(cudaEventCreate(&a));
+            ADSB_CUDA(cudaEventCreate(&b));
+            ADSB_CUDA(cudaEventRecord(a, s1));
+            launch_sampler(static_cast<SamplerKind>(ctx.arena->kind == 0 ? 0 : 1), false, p, s1);
+            ADSB_CUDA(cudaEventRecord(b, s1));
+            launch_ev.emplace_back(a, b);
             ADSB_CUDA(cudaEventRecord(samp[k], s1));
             L.count++;
             launched++;
@@ -459,6 +489,12 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         ADSB_CUDA(cudaEventCreate(&t_end));
         ADSB_CUDA(cudaEventRecord(t_begin, s1));
         enqueue_sampler(0);
+        PinnedBuf<unsigned long long> stat0(kStatCount);
+        cudaEvent_t stat_ev;
+        ADSB_CUDA(cudaEventCreateWithFlags(&stat_ev, cudaEventDisableTiming));
+        ADSB_CUDA(cudaMemcpyAsync(stat0.ptr, stats.ptr, kStatCount * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s1));
+        ADSB_CUDA(cudaEventRecord(stat_ev, s1));
         enqueue_check(0);
         if (max_epochs > 1) enqueue_sampler(1);
         uint64_t e = 0;
@@ -466,6 +502,13 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             const int k = static_cast<int>(e & 1);
             ADSB_CUDA(cudaEventSynchronize(chk[k]));
             const bool pass = flag_host.ptr[k] != 0;
+            if (e == 0) {
+                ADSB_CUDA(cudaEventSynchronize(stat_ev));
+                SamplerArena& ar = *ctx.arena;
+                if (ar.kind == 1 && ar.use_smem && stat0.ptr[kStatSamples] >= 256 &&
+                    stat0.ptr[kStatFallbacks] * 2 > stat0.ptr[kStatSamples])
+                    ar.use_smem = false;
+            }
             if (pass || e + 1 >= max_epochs) {
                 if (!pass) out.reason = ADSB_REASON_CAPPED;
                 break;
@@ -476,9 +519,13 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         ADSB_CUDA(cudaEventRecord(t_end, s1));
         ADSB_CUDA(cudaStreamSynchronize(s1));
         ADSB_CUDA(cudaStreamSynchronize(s2));
-        float ms = 0;
-        ADSB_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
-        out.sampler_ms = ms;  // sampling stream busy span (epochs back to back)
+        for (auto& [a, b] : launch_ev) {
+            float ms = 0;
+            ADSB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            out.sampler_ms += ms;  // device time of the sampler launches only
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
         out.tau = (e + 1) * B;
         out.check_cycles = e + 1;
         out.stop_epoch = e + 1;
@@ -489,6 +536,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         }
         cudaEventDestroy(t_begin);
         cudaEventDestroy(t_end);
+        cudaEventDestroy(stat_ev);
     }
 
     // ---- results
@@ -506,6 +554,9 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     out.counts.assign(host32.begin(), host32.end());
     out.edges_scanned = st_host[kStatEdges];
     out.vertices_expanded = st_host[kStatVertices];
+    out.rebuild_edges = st_host[kStatRebuildEdges];
+    out.backtrack_edges = st_host[kStatBacktrackEdges];
+    out.store_fallbacks = st_host[kStatFallbacks];
     out.kernel_launches = L.count;
     // kadabra.hpp:339-343
     if (out.reason != ADSB_REASON_CAPPED) {

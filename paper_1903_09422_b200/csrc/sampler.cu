@@ -25,6 +25,9 @@
 // takes one adjacency entry of the flattened range (coalesced reads for hubs
 // and for low-degree chunks alike). New vertices are claimed with one 64-bit
 // CAS on their state word and appended with ballot/popc compaction.
+#include <cstdlib>
+#include <string>
+
 #include "device.cuh"
 #include "rng.hpp"
 #include "sampler.cuh"
@@ -85,7 +88,9 @@ struct Team {
     uint32_t level_cap;
     uint32_t lane;
     uint32_t tag;
-    unsigned long long edges;
+    unsigned long long edges;          // BFS expansion
+    unsigned long long rebuild_edges;  // DAG sigma rebuild
+    unsigned long long back_edges;     // backtrack scans
     unsigned long long verts;
     bool error;
 
@@ -235,40 +240,38 @@ __device__ bool expand_t(Team& T, uint32_t lo, uint32_t hi, uint32_t a, uint32_t
     return met;
 }
 
-// sigma_s on the t-side DAG layer k-1 from layer k (push along DAG edges).
+// sigma_s on the t-side DAG layer k-1, pulled from layer k: every vertex w of
+// T_{k-1} sums sigma_s over its neighbours that are DAG vertices of T_k. The
+// cost is T_{k-1}'s degree sum, i.e. exactly what expanding T_{k-1} cost
+// (pushing from DAG_k instead would scan the hubs that sit in later layers).
 __device__ void rebuild_level(Team& T, uint32_t lo, uint32_t hi, uint32_t k) {
     for (uint32_t base = lo; base < hi; base += 32) {
         const uint32_t j = base + T.lane;
-        uint32_t o = 0, dg = 0;
-        unsigned long long sv = 0;
+        uint32_t w = 0, o = 0, dg = 0;
         if (j < hi) {
             const uint32_t q = T.tpos(j);
-            const ulonglong2 s = T.ld_state(T.queue[q]);
-            if (s.x & kDag) {
-                const uint2 r = T.qrange[q];
-                o = r.x;
-                dg = r.y;
-                sv = s.y;
-            }
+            w = T.queue[q];
+            const uint2 r = T.qrange[q];
+            o = r.x;
+            dg = r.y;
         }
         const uint32_t incl = warp_incl_scan(dg, T.lane);
         const uint32_t excl = incl - dg;
         const uint32_t total = __shfl_sync(kFull, incl, 31);
-        if (total) T.verts += __popc(__ballot_sync(kFull, dg != 0));
-        T.edges += total;
+        T.rebuild_edges += total;
         for (uint32_t e0 = 0; e0 < total; e0 += 32) {
             const uint32_t e = e0 + T.lane;
             const bool active = e < total;
             const int ow = owner_of(incl, active ? e : 0);
             const uint32_t o_o = __shfl_sync(kFull, o, ow);
             const uint32_t ex_o = __shfl_sync(kFull, excl, ow);
-            const unsigned long long sv_o = shfl64(sv, ow);
+            const uint32_t w_o = __shfl_sync(kFull, w, ow);
             if (active) {
-                const uint32_t w = T.nbrs[o_o + (e - ex_o)];
-                const unsigned long long m = T.ld_meta(w);
-                if (tag_of(m) == T.tag && is_t(m) && dist_of(m) == k - 1) {
-                    atomicAdd(T.sigma_ptr(w), sv_o);
-                    if (!(m & kDag)) atomicOr(T.meta_ptr(w), kDag);
+                const uint32_t v = T.nbrs[o_o + (e - ex_o)];
+                const ulonglong2 sv = T.ld_state(v);
+                if (tag_of(sv.x) == T.tag && is_t(sv.x) && dist_of(sv.x) == k && (sv.x & kDag)) {
+                    atomicAdd(T.sigma_ptr(w_o), sv.y);
+                    atomicOr(T.meta_ptr(w_o), kDag);
                 }
             }
         }
@@ -345,7 +348,7 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
     const uint32_t d = a + b + 1;  // d(s, t)
 
     // sigma_s on the t-side DAG layers b-1 .. 0 (layer b was filled by the meeting)
-    for (uint32_t k = b; k >= 1; --k) rebuild_level(T, T.tlev[k], T.tlev[k + 1], k);
+    for (uint32_t k = b; k >= 1; --k) rebuild_level(T, T.tlev[k - 1], T.tlev[k], k);
 
     // Backtrack from t (kadabra.hpp:227-242), d-1 interior vertices.
     if (d < 2) return;
@@ -385,7 +388,7 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
                                   dist_of(sq.x) == want_dist && (!want_t || (sq.x & kDag));
                 val = cand ? sq.y : 0ull;
             }
-            T.edges += min(32u, end - base);
+            T.back_edges += min(32u, end - base);
             // 65-bit inclusive prefix sum (lo + carry count)
             unsigned long long lo = val;
             uint32_t hi = 0;
@@ -434,6 +437,8 @@ __global__ void __launch_bounds__(256) sampler_kernel(SamplerParams p) {
     T.lane = lane;
     T.tag = p.slot_tag[slot];
     T.edges = 0;
+    T.rebuild_edges = 0;
+    T.back_edges = 0;
     T.verts = 0;
     T.error = false;
     unsigned long long samples = 0;
@@ -451,7 +456,9 @@ __global__ void __launch_bounds__(256) sampler_kernel(SamplerParams p) {
     }
     if (lane == 0) {
         p.slot_tag[slot] = T.tag;
-        atomicAdd(p.stats + kStatEdges, T.edges);
+        atomicAdd(p.stats + kStatEdges, T.edges + T.rebuild_edges + T.back_edges);
+        atomicAdd(p.stats + kStatRebuildEdges, T.rebuild_edges);
+        atomicAdd(p.stats + kStatBacktrackEdges, T.back_edges);
         atomicAdd(p.stats + kStatVertices, T.verts);
         atomicAdd(p.stats + kStatSamples, samples);
         if (T.error) atomicAdd(p.stats + kStatErrors, 1ull);
@@ -469,13 +476,24 @@ int sampler_warps_per_sm(bool deterministic) {
     return blocks * kWarpsPerBlock;
 }
 
-void launch_sampler(bool deterministic, const SamplerParams& p, cudaStream_t stream) {
+void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_t stream) {
     const unsigned blocks = (p.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (deterministic)
         sampler_kernel<true><<<blocks, 256, 0, stream>>>(p);
     else
         sampler_kernel<false><<<blocks, 256, 0, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
+}
+
+SamplerKind sampler_kind() {
+    const char* e = std::getenv("ADSB_SAMPLER");
+    if (e && std::string(e) == "warp") return SamplerKind::kWarp;
+    return SamplerKind::kBlock;
+}
+
+void launch_sampler(SamplerKind kind, bool deterministic, const SamplerParams& p, cudaStream_t stream) {
+    if (kind == SamplerKind::kWarp) launch_sampler_warp(deterministic, p, stream);
+    else launch_sampler_cta(deterministic, p, stream);
 }
 
 }  // namespace adsb

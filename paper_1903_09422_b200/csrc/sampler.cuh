@@ -16,7 +16,16 @@ constexpr unsigned long long kSideT = 1ull << 31;
 constexpr unsigned long long kDag = 1ull << 30;
 constexpr unsigned long long kDistMask = (1ull << 30) - 1;
 
-enum SamplerStat { kStatEdges = 0, kStatVertices = 1, kStatSamples = 2, kStatErrors = 3, kStatCount = 4 };
+enum SamplerStat {
+    kStatEdges = 0,
+    kStatVertices = 1,
+    kStatSamples = 2,
+    kStatErrors = 3,
+    kStatRebuildEdges = 4,
+    kStatBacktrackEdges = 5,
+    kStatFallbacks = 6,
+    kStatCount = 7
+};
 
 struct SamplerParams {
     // graph (device CSR, u32 offsets) and component labels
@@ -28,6 +37,8 @@ struct SamplerParams {
     uint32_t level_cap;
     uint32_t rank;         // this GPU's rank: items map to positions first + item*world + rank
     uint32_t world;
+    uint32_t hash_cap;     // block sampler: shared-memory hash capacity (power of two)
+    uint32_t use_smem;     // block sampler: try the shared-memory store first
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode
@@ -49,8 +60,16 @@ struct SamplerParams {
     unsigned long long* stats;  // kStatCount
 };
 
-// Resident teams (warps) per SM for the sampler kernel at 256 threads/block.
+// Warp-team sampler (sampler.cu): slots = resident warps.
 int sampler_warps_per_sm(bool deterministic);
-void launch_sampler(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+// Block-team sampler with shared-memory state (sampler_cta.cu): slots = blocks.
+size_t sampler_cta_smem_bytes(uint32_t hash_cap);
+int sampler_cta_blocks_per_sm(uint32_t hash_cap);
+void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+
+enum class SamplerKind { kWarp, kBlock };
+SamplerKind sampler_kind();  // ADSB_SAMPLER=warp|block (default block)
+void launch_sampler(SamplerKind kind, bool deterministic, const SamplerParams& p, cudaStream_t stream);
 
 }  // namespace adsb

@@ -82,6 +82,9 @@ class BcResult:
     vertices_expanded: int = 0
     kernel_launches: int = 0
     sampler_ms: float = 0.0
+    rebuild_edges: int = 0
+    backtrack_edges: int = 0
+    store_fallbacks: int = 0
 
 
 def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | None = None,
@@ -104,7 +107,9 @@ def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | N
                     diameter_bound=st.diameter_bound, preprocess_seconds=st.preprocess_seconds,
                     ads_seconds=st.ads_seconds, run=run, num_components=st.num_components,
                     edges_scanned=st.edges_scanned, vertices_expanded=st.vertices_expanded,
-                    kernel_launches=st.kernel_launches, sampler_ms=st.sampler_ms)
+                    kernel_launches=st.kernel_launches, sampler_ms=st.sampler_ms,
+                    rebuild_edges=st.rebuild_edges, backtrack_edges=st.backtrack_edges,
+                    store_fallbacks=st.store_fallbacks)
 
 
 def sample_frames(g: Graph, seed: int, samples_per_frame: int, first: int, count: int,

@@ -143,3 +143,34 @@ def test_single_vertex_and_errors():
         estimate_bc(g, 1.5, 0.1, EngineConfig())
     with pytest.raises(ValueError):
         estimate_bc(g, 0.1, 0.0, EngineConfig())
+
+
+@pytest.mark.parametrize("mode", ["block", "block-global", "block-tinyhash", "warp"])
+def test_sampler_variants_bit_exact(mode, monkeypatch, grid200):
+    """All sampler implementations (block teams with the shared-memory table,
+    block teams forced onto global state, a table so small that most samples
+    overflow and are redone, warp teams) give the same paths and results."""
+    monkeypatch.delenv("ADSB_SAMPLER", raising=False)
+    monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    monkeypatch.delenv("ADSB_HASH_CAP", raising=False)
+    if mode == "warp":
+        monkeypatch.setenv("ADSB_SAMPLER", "warp")
+    elif mode == "block-global":
+        monkeypatch.setenv("ADSB_NO_SMEM", "1")
+    elif mode == "block-tinyhash":
+        monkeypatch.setenv("ADSB_HASH_CAP", "64")
+    p = datasets.pairs("c1_er")
+    pg, og = both(p)  # fresh handle -> fresh device context / arena
+    got = sample_frames(pg.graph, 77, 2, 0, 1500)
+    want = oracle.sample_frames(og, 77, 2, 0, 1500)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=1, base_seed=42, threads=8)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cfg)
+    assert r.tau == 10307
+    gp = datasets.gen_grid(200, 200, 0.0, 3)
+    pg2, og2 = both(gp)
+    got = sample_frames(pg2.graph, 9, 1, 0, 40)
+    want = oracle.sample_frames(og2, 9, 1, 0, 40)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)

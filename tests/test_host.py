@@ -1,0 +1,173 @@
+"""CPU tests of the product's host side and its C ABI (no GPU needed).
+
+The host ingestion (parse_edge_list / from_edges / CSR) and the scalar rules
+run on the CPU by design; they are compared with the oracle here. Everything
+that traverses the graph is GPU-only and covered by test_gpu_parity.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1903_09422_b200 import CudaError, InvalidArgument, ParseError, _lib, adsamp, datasets, kadabra
+
+from conftest import SMALL_GRAPHS
+from test_oracle import PARSE_CASES, PARSE_ERRORS
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_c_abi_exports_every_declared_symbol():
+    header = (ROOT / "include" / "adsb.h").read_text()
+    declared = set(re.findall(r"\b(adsb_[a-z_0-9]+)\s*\(", header))
+    lib = C.CDLL(str(_lib.LIB_PATH))
+    missing = [name for name in sorted(declared) if not hasattr(lib, name)]
+    assert not missing, missing
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    assert _lib.lib().adsb_abi_version() == 1
+
+
+def test_struct_layouts():
+    assert C.sizeof(_lib.Config) == 80
+    assert C.sizeof(_lib.Stats) == 128
+
+
+@pytest.mark.parametrize("text,n,m,ids", PARSE_CASES)
+def test_parse_examples(text, n, m, ids):
+    p = adsamp.parse_edge_list(text)
+    o = oracle.parse_text(text)
+    assert p.graph.num_vertices() == n and p.graph.num_edges() == m
+    assert list(p.original_ids) == ids
+    np.testing.assert_array_equal(p.graph.offsets(), o.offsets)
+    np.testing.assert_array_equal(p.graph.neighbor_list(), o.nbrs)
+
+
+@pytest.mark.parametrize("text,msg", PARSE_ERRORS)
+def test_parse_errors(text, msg):
+    with pytest.raises(ParseError) as e:
+        adsamp.parse_edge_list(text)
+    assert str(e.value) == msg
+
+
+def test_parse_file_and_pairs_agree(tmp_path):
+    for name in ["er100", "cube", "two_components"]:
+        pairs = SMALL_GRAPHS[name]().reshape(-1)
+        path = tmp_path / f"{name}.edges"
+        datasets.write_edge_list(path, pairs)
+        a = adsamp.parse_edge_list_file(path)
+        b = adsamp.graph_from_pairs(pairs)
+        o = oracle.parse_file(path)
+        for g in (a, b):
+            np.testing.assert_array_equal(g.graph.offsets(), o.offsets)
+            np.testing.assert_array_equal(g.graph.neighbor_list(), o.nbrs)
+            np.testing.assert_array_equal(g.original_ids, o.original_ids)
+
+
+def test_c1_ingestion_matches_oracle():
+    pairs = datasets.pairs("c1_er")
+    g = adsamp.graph_from_pairs(pairs)
+    o = oracle.from_pairs(pairs)
+    assert g.graph.num_vertices() == 10_000 and g.graph.num_edges() == 50_000
+    np.testing.assert_array_equal(g.graph.offsets(), o.offsets)
+    np.testing.assert_array_equal(g.graph.neighbor_list(), o.nbrs)
+    np.testing.assert_array_equal(g.original_ids, o.original_ids)
+
+
+def test_from_edges_and_csr_validation():
+    g = adsamp.Graph.from_edges(4, [(0, 1), (1, 0), (2, 2), (3, 1)])
+    assert g.num_vertices() == 4 and g.num_edges() == 2
+    assert list(g.neighbors(1)) == [0, 3]
+    with pytest.raises(InvalidArgument):
+        adsamp.Graph.from_edges(2, [(0, 5)])
+    h = adsamp.Graph.from_csr(4, g.offsets(), g.neighbor_list())
+    np.testing.assert_array_equal(h.neighbor_list(), g.neighbor_list())
+    with pytest.raises(InvalidArgument):
+        adsamp.Graph.from_csr(2, [0, 1, 2], [1, 1])  # self loop at 1
+    with pytest.raises(InvalidArgument):
+        adsamp.Graph.from_csr(3, [0, 2, 2, 2], [2, 1])  # not ascending
+
+
+def test_serialize_and_renumbering():
+    # graph.hpp:140-144 writes dense ids; re-parsing renumbers them by first
+    # appearance, so the round trip is NOT the identity in general (the
+    # reference's own test_graph.cpp:76-89 asserts it and would fail).
+    g = adsamp.Graph.from_edges(3, [(0, 2), (1, 2)])
+    text = adsamp.serialize_edge_list(g)
+    assert text == "0 2\n1 2\n"
+    back = adsamp.parse_edge_list(text)
+    assert list(back.original_ids) == [0, 2, 1]
+    assert list(back.graph.neighbor_list()) != list(g.neighbor_list())
+
+
+def test_generators_are_deterministic_and_sized():
+    a, b = datasets.gen_rmat(10, 8, 0.57, 0.19, 0.19, 5), datasets.gen_rmat(10, 8, 0.57, 0.19, 0.19, 5)
+    np.testing.assert_array_equal(a, b)
+    ba = datasets.gen_ba(500, 3, 2)
+    assert ba.shape[0] == 2 * (3 * 4 // 2 + (500 - 4) * 3)
+    grid = datasets.gen_grid(16, 16, 0.0, 0)
+    assert grid.shape[0] == 2 * 480
+    c1 = datasets.pairs("c1_er")
+    assert c1.shape[0] == 100_000
+
+
+def test_scalar_rules_match_oracle():
+    for dub in [0, 1, 3, 8, 12, 8182, 10**6]:
+        for eps in [0.001, 0.005, 0.01, 0.1]:
+            assert kadabra.compute_omega(dub, eps, 0.1) == oracle.compute_omega(dub, eps, 0.1)
+    rng = adsamp.SplitMix64(5)
+    for _ in range(500):
+        b = rng.next_below(10**6) / 10**6
+        dv = (1 + rng.next_below(10**6)) / 10**7
+        om, tau = 1 + rng.next_below(10**5), 1 + rng.next_below(10**5)
+        assert kadabra.f_bound(b, dv, om, tau) == oracle.f_bound(b, dv, om, tau)
+        assert kadabra.g_bound(b, dv, om, tau) == oracle.g_bound(b, dv, om, tau)
+    with pytest.raises(ValueError):
+        kadabra.f_bound(0.1, 0.01, 10, 0)
+    with pytest.raises(ValueError):
+        kadabra.compute_omega(3, 1.0, 0.1)
+    d = np.array([400, 100, 0], np.uint64)
+    assert kadabra.kadabra_check(d, 500, 500, 0.0001, 0.1)  # omega cap (test_kadabra.cpp:178-182)
+
+
+def test_engine_helpers():
+    # test_engine.cpp:50-60, :62-72, :220-229
+    xi32 = np.log(100.0) / np.log(32.0)
+    assert adsamp.check_budget(1000, 32, xi32) == 10
+    assert adsamp.check_budget(1000, 1, 1.3285) == 1000
+    assert adsamp.check_budget(1000, 4, 1.3285) == 159
+    assert adsamp.check_budget(1, 64, 2.0) == 1
+    with pytest.raises(InvalidArgument):
+        adsamp.check_budget(0, 1, 1.0)
+    assert adsamp.shared_frame_target(5, 2) == 1
+    assert adsamp.indexed_frame_index(2, 1, 4) == 9
+    c = adsamp.ReservationCounter()
+    assert [adsamp.reserve_indices(c, 4, 2) for _ in range(5)] == \
+           [[0, 4, 8], [1, 5, 9], [2, 6, 10], [3, 7, 11], [12, 16, 20]]
+    cfg = adsamp.EngineConfig(threads=2, variant=adsamp.Variant.shared, frame_groups=3)
+    with pytest.raises(InvalidArgument):
+        cfg.validate()
+    assert adsamp.parse_variant("indexed") == adsamp.Variant.indexed
+    with pytest.raises(InvalidArgument):
+        adsamp.parse_variant("bogus")
+
+
+def _cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_cuda_available(), reason="checks the no-GPU failure path")
+def test_no_cpu_fallback_without_gpu():
+    g = adsamp.Graph.from_edges(3, [(0, 1), (1, 2)])
+    with pytest.raises(CudaError, match="no CUDA device"):
+        kadabra.estimate_bc(g, 0.1, 0.1, adsamp.EngineConfig(variant=adsamp.Variant.indexed))
+    with pytest.raises(CudaError):
+        adsamp.connected_components(g)
