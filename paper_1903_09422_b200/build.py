@@ -22,6 +22,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libadsb.so"
+TOOL = PKG / "adsb_run"
+TOOL_SRC = ROOT / "tools" / "adsb_run.cpp"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [
@@ -77,6 +79,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}\n{res.stdout}")
+    if TOOL_SRC.exists() and (not TOOL.exists() or TOOL.stat().st_mtime < max(LIB.stat().st_mtime,
+                                                                            TOOL_SRC.stat().st_mtime)):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++20", f"-I{ROOT / 'include'}", str(TOOL_SRC),
+               "-o", str(TOOL), f"-L{PKG}", "-ladsb", "-Wl,-rpath,$ORIGIN"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"adsb_run build failed:\n{res.stderr}")
     if verbose:
         for log in logs:
             if log.strip():

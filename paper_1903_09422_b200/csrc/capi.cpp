@@ -36,6 +36,17 @@ DeviceContext& context_for(const adsb_graph* cg, int requested) {
     return *it->second;
 }
 
+// The device runtime (streams, scratch, arenas) is shared by all graphs on a
+// device: engine calls on one device are serialised.
+struct Locked {
+    DeviceContext& ctx;
+    std::unique_lock<std::mutex> lock;
+};
+Locked locked_context(const adsb_graph* g, int requested) {
+    DeviceContext& ctx = context_for(g, requested);
+    return {ctx, std::unique_lock<std::mutex>(ctx.rt->mu)};
+}
+
 adsb_graph* wrap(HostGraph&& h) {
     auto* g = new adsb_graph;
     g->host = std::move(h);
@@ -170,8 +181,8 @@ adsb_status adsb_connected_components(const adsb_graph* g, int device, uint32_t*
                                       uint32_t* num_components) {
     return guard([&] {
         need(g, "graph");
-        DeviceContext& ctx = context_for(g, device);
-        ctx.labels_ready = false;
+        Locked L = locked_context(g, device);
+        DeviceContext& ctx = L.ctx;
         const uint32_t c = device_components(ctx);
         if (num_components) *num_components = c;
         if (labels && g->host.n)
@@ -183,8 +194,8 @@ adsb_status adsb_eccentricity(const adsb_graph* g, int device, uint32_t source, 
     return guard([&] {
         need(g, "graph");
         need(out, "out");
-        DeviceContext& ctx = context_for(g, device);
-        *out = device_eccentricity(ctx, source);
+        Locked L = locked_context(g, device);
+        *out = device_eccentricity(L.ctx, source);
     });
 }
 
@@ -192,9 +203,8 @@ adsb_status adsb_diameter_upper_bound(const adsb_graph* g, int device, uint64_t*
     return guard([&] {
         need(g, "graph");
         need(out, "out");
-        DeviceContext& ctx = context_for(g, device);
-        ctx.labels_ready = false;
-        *out = g->host.n == 0 ? 0 : device_diameter_bound(ctx);
+        Locked L = locked_context(g, device);
+        *out = g->host.n == 0 ? 0 : device_diameter_bound(L.ctx);
     });
 }
 
@@ -291,8 +301,8 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
         opt.comm = cfg->comm;
         int device = cfg->device;
         if (cfg->comm) device = cfg->comm->device;
-        DeviceContext& ctx = context_for(g, device);
-        EngineOutput r = adsb::estimate_bc(ctx, epsilon, delta, opt);
+        Locked L = locked_context(g, device);
+        EngineOutput r = adsb::estimate_bc(L.ctx, epsilon, delta, opt);
         const uint32_t n = g->host.n;
         for (uint32_t v = 0; v < n; ++v) {
             if (counts) counts[v] = r.counts[v];
@@ -328,9 +338,8 @@ adsb_status adsb_sample_frames(const adsb_graph* g, int device, uint64_t seed, u
         need(frame_offsets, "frame_offsets");
         if (cap) need(incs, "incs");
         if (g->host.n < 2) invalid("sampling needs at least two vertices");
-        DeviceContext& ctx = context_for(g, device);
-        ctx.labels_ready = false;
-        sample_frames(ctx, seed, spf, first, count, frame_offsets, incs, cap);
+        Locked L = locked_context(g, device);
+        sample_frames(L.ctx, seed, spf, first, count, frame_offsets, incs, cap);
     });
 }
 

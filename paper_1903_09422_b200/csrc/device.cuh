@@ -3,8 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -59,6 +61,15 @@ struct PinnedBuf {
     T* ptr = nullptr;
     size_t count = 0;
     PinnedBuf() = default;
+    PinnedBuf(PinnedBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+    PinnedBuf& operator=(PinnedBuf&& o) noexcept {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = o.ptr;
+        count = o.count;
+        o.ptr = nullptr;
+        o.count = 0;
+        return *this;
+    }
     explicit PinnedBuf(size_t n) {
         if (n == 0) n = 1;
         ADSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
@@ -69,6 +80,28 @@ struct PinnedBuf {
     ~PinnedBuf() {
         if (ptr) cudaFreeHost(ptr);
     }
+};
+
+// Reusable per-context scratch: buffers grow on demand and are kept between
+// calls, so a steady-state estimate_bc performs no cudaMalloc/cudaFree (which
+// would synchronise the device) and no pinned-host allocation.
+enum class Scratch : int {
+    kParent, kIsRoot, kRank, kCubTemp, kFlags, kDist, kFrontA, kFrontB, kLevelCounts, kBest,
+    kTotal, kStats, kScal, kBaseMax, kStopIdx, kEvents, kSorted, kGathered, kFrameMax, kRunMax,
+    kSortTemp, kEpochCnt, kDmax, kFlagDev, kTickets, kNcclScalar, kCount
+};
+
+struct ScratchPool {
+    DevBuf<uint8_t> dev[static_cast<int>(Scratch::kCount)];
+    template <class T>
+    T* get(Scratch id, size_t count) {
+        DevBuf<uint8_t>& b = dev[static_cast<int>(id)];
+        const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+        if (b.count < bytes) b.alloc(bytes + bytes / 4 + 256);
+        return reinterpret_cast<T*>(b.ptr);
+    }
+    template <class T>
+    size_t capacity(Scratch id) const { return dev[static_cast<int>(id)].count / sizeof(T); }
 };
 
 struct DeviceGraph {
@@ -86,6 +119,7 @@ struct SamplerArena {
     int kind = 1;            // SamplerKind (0 warp teams, 1 block teams)
     uint32_t hash_cap = 0;   // block teams: shared-memory hash capacity
     bool use_smem = true;    // block teams: disabled when most samples overflow the table
+    uint32_t block_threads = 256;
     uint32_t slots = 0;
     uint32_t n = 0;
     uint32_t level_cap = 0;
@@ -96,16 +130,37 @@ struct SamplerArena {
     DevBuf<uint32_t> slot_tag;         // slots
 };
 
+// Process-wide per-device runtime shared by every graph handle on that
+// device: streams, events, the scratch pool, pinned staging and the sampler
+// arenas. Creating a graph therefore costs only its CSR upload. Calls that use
+// the runtime hold `mu` (one engine call per device at a time).
+struct DeviceRuntime {
+    int device = 0;
+    std::mutex mu;
+    std::unique_ptr<SamplerArena> arena[2];    // per SamplerKind
+    int active = 1;                            // arena used by the current call
+    ScratchPool pool;
+    PinnedBuf<unsigned long long> pinned;      // 128 words of small host staging (level counts, flags, stats)
+    PinnedBuf<uint32_t> host_counts;           // result download
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_stat = nullptr;
+    cudaEvent_t ev_samp[2] = {nullptr, nullptr}, ev_chk[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_launch;
+    cudaStream_t stream = nullptr;   // sampling stream
+    cudaStream_t stream2 = nullptr;  // check / collective stream
+};
+
+// Never destroyed: lives until process exit (CUDA tears its resources down then).
+DeviceRuntime& device_runtime(int device);
+
 struct DeviceContext {
     int device = 0;
     DeviceGraph graph;
     DevBuf<uint32_t> labels;  // component labels (reference numbering)
     bool labels_ready = false;
+    bool dub_ready = false;   // the graph is immutable: labels and D_ub are computed once per handle
+    uint64_t diameter_bound = 0;
     uint32_t num_components = 0;
-    std::unique_ptr<SamplerArena> arena;
-    cudaStream_t stream = nullptr;   // sampling stream
-    cudaStream_t stream2 = nullptr;  // check / collective stream
-    ~DeviceContext();
+    DeviceRuntime* rt = nullptr;
 };
 
 int resolve_device(int requested);

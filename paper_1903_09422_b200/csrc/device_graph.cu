@@ -14,6 +14,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "device.cuh"
 
@@ -142,9 +144,21 @@ int resolve_device(int requested) {
     return dev;
 }
 
-DeviceContext::~DeviceContext() {
-    if (stream) cudaStreamDestroy(stream);
-    if (stream2) cudaStreamDestroy(stream2);
+DeviceRuntime& device_runtime(int device) {
+    static std::mutex mu;
+    static std::map<int, DeviceRuntime*> runtimes;  // intentionally leaked (see device.cuh)
+    std::lock_guard<std::mutex> lock(mu);
+    DeviceRuntime*& rt = runtimes[device];
+    if (!rt) {
+        ADSB_CUDA(cudaSetDevice(device));
+        auto* r = new DeviceRuntime;
+        r->device = device;
+        ADSB_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+        ADSB_CUDA(cudaStreamCreateWithFlags(&r->stream2, cudaStreamNonBlocking));
+        r->pinned = PinnedBuf<unsigned long long>(128);
+        rt = r;
+    }
+    return *rt;
 }
 
 std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int device) {
@@ -152,8 +166,8 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
     ADSB_CUDA(cudaSetDevice(device));
     auto ctx = std::make_unique<DeviceContext>();
     ctx->device = device;
-    ADSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    ADSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    ctx->rt = &device_runtime(device);
+    std::lock_guard<std::mutex> lock(ctx->rt->mu);
     DeviceGraph& dg = ctx->graph;
     dg.device = device;
     dg.n = g.n;
@@ -164,11 +178,11 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
     dg.offsets.alloc(off32.size());
     dg.nbrs.alloc(std::max<uint64_t>(1, g.nnz()));
     ADSB_CUDA(cudaMemcpyAsync(dg.offsets.ptr, off32.data(), off32.size() * sizeof(uint32_t),
-                              cudaMemcpyHostToDevice, ctx->stream));
+                              cudaMemcpyHostToDevice, ctx->rt->stream));
     if (g.nnz())
         ADSB_CUDA(cudaMemcpyAsync(dg.nbrs.ptr, g.nbrs.data(), g.nnz() * sizeof(uint32_t),
-                                  cudaMemcpyHostToDevice, ctx->stream));
-    ADSB_CUDA(cudaStreamSynchronize(ctx->stream));
+                                  cudaMemcpyHostToDevice, ctx->rt->stream));
+    ADSB_CUDA(cudaStreamSynchronize(ctx->rt->stream));
     return ctx;
 }
 
@@ -181,27 +195,27 @@ static unsigned grid_for(uint64_t work, int device, unsigned block = 256) {
 uint32_t device_components(DeviceContext& ctx) {
     if (ctx.labels_ready) return ctx.num_components;
     const uint32_t n = ctx.graph.n;
-    cudaStream_t s = ctx.stream;
-    DevBuf<uint32_t> parent(n), is_root(n), rank(n + 1);
-    ctx.labels.alloc(n);
+    cudaStream_t s = ctx.rt->stream;
+    uint32_t* parent = ctx.rt->pool.get<uint32_t>(Scratch::kParent, n);
+    uint32_t* is_root = ctx.rt->pool.get<uint32_t>(Scratch::kIsRoot, n + 1);  // zero tail: scanned with n+1 inputs
+    uint32_t* rank = ctx.rt->pool.get<uint32_t>(Scratch::kRank, n + 1);
+    if (ctx.labels.count < n) ctx.labels.alloc(n);
     const unsigned g = grid_for(n, ctx.device);
-    uf_init<<<g, 256, 0, s>>>(parent.ptr, n);
+    uf_init<<<g, 256, 0, s>>>(parent, n);
     uf_hook<<<grid_for(static_cast<uint64_t>(n) * 32, ctx.device), 256, 0, s>>>(
-        ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent.ptr, n);
-    uf_compress<<<g, 256, 0, s>>>(parent.ptr, is_root.ptr, n);
+        ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent, n);
+    uf_compress<<<g, 256, 0, s>>>(parent, is_root, n);
+    ADSB_CUDA(cudaMemsetAsync(is_root + n, 0, sizeof(uint32_t), s));
     size_t temp_bytes = 0;
-    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, is_root.ptr, rank.ptr, n + 1, s));
-    DevBuf<uint8_t> temp(temp_bytes);
-    // rank has n+1 entries: scanning n+1 inputs reads is_root[n]; give it a zero tail
-    DevBuf<uint32_t> flags(n + 1);
-    ADSB_CUDA(cudaMemsetAsync(flags.ptr + n, 0, sizeof(uint32_t), s));
-    ADSB_CUDA(cudaMemcpyAsync(flags.ptr, is_root.ptr, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(temp.ptr, temp_bytes, flags.ptr, rank.ptr, n + 1, s));
-    uf_label<<<g, 256, 0, s>>>(parent.ptr, rank.ptr, ctx.labels.ptr, n);
-    uint32_t comps = 0;
-    ADSB_CUDA(cudaMemcpyAsync(&comps, rank.ptr + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, is_root, rank, n + 1, s));
+    uint8_t* temp = ctx.rt->pool.get<uint8_t>(Scratch::kCubTemp, temp_bytes);
+    ADSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, is_root, rank, n + 1, s));
+    uf_label<<<g, 256, 0, s>>>(parent, rank, ctx.labels.ptr, n);
+    uint32_t* comps_h = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr);
+    ADSB_CUDA(cudaMemcpyAsync(comps_h, rank + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     ADSB_CUDA(cudaStreamSynchronize(s));
     ADSB_CUDA(cudaGetLastError());
+    const uint32_t comps = *comps_h;
     ctx.num_components = comps;
     ctx.labels_ready = true;
     return comps;
@@ -210,24 +224,23 @@ uint32_t device_components(DeviceContext& ctx) {
 // Level-synchronous BFS from `sources` (already written into frontier A with
 // dist 0); returns the deepest non-empty level. Levels are launched in
 // chunks so the host synchronises once per chunk, not once per level.
-static uint64_t bfs_depth(DeviceContext& ctx, DevBuf<uint32_t>& dist, DevBuf<uint32_t>& fa,
-                          DevBuf<uint32_t>& fb, DevBuf<uint32_t>& counts) {
+static uint64_t bfs_depth(DeviceContext& ctx, uint32_t* dist, uint32_t* fa, uint32_t* fb, uint32_t* counts) {
     const uint32_t n = ctx.graph.n;
-    cudaStream_t s = ctx.stream;
+    cudaStream_t s = ctx.rt->stream;
     const unsigned grid = static_cast<unsigned>(num_sms(ctx.device) * 8);
     constexpr uint32_t kChunk = 32;
     uint32_t level = 0;
-    std::vector<uint32_t> host(kChunk);
+    uint32_t* host = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr);  // 64 words of pinned staging
     for (;;) {
         for (uint32_t k = 0; k < kChunk && level + k + 1 <= n; ++k) {
             const uint32_t L = level + k;
-            uint32_t* fin = (L & 1) ? fb.ptr : fa.ptr;
-            uint32_t* fout = (L & 1) ? fa.ptr : fb.ptr;
-            bfs_level<<<grid, 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, dist.ptr, fin,
-                                           counts.ptr + L, fout, counts.ptr + L + 1, L);
+            uint32_t* fin = (L & 1) ? fb : fa;
+            uint32_t* fout = (L & 1) ? fa : fb;
+            bfs_level<<<grid, 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, dist, fin, counts + L, fout,
+                                           counts + L + 1, L);
         }
         const uint32_t avail = std::min<uint32_t>(kChunk, n - level);
-        ADSB_CUDA(cudaMemcpyAsync(host.data(), counts.ptr + level + 1, avail * sizeof(uint32_t),
+        ADSB_CUDA(cudaMemcpyAsync(host, counts + level + 1, avail * sizeof(uint32_t),
                                   cudaMemcpyDeviceToHost, s));
         ADSB_CUDA(cudaStreamSynchronize(s));
         ADSB_CUDA(cudaGetLastError());
@@ -241,29 +254,39 @@ static uint64_t bfs_depth(DeviceContext& ctx, DevBuf<uint32_t>& dist, DevBuf<uin
 uint64_t device_eccentricity(DeviceContext& ctx, uint32_t source) {
     const uint32_t n = ctx.graph.n;
     if (source >= n) invalid("source vertex out of range");
-    cudaStream_t s = ctx.stream;
-    DevBuf<uint32_t> dist(n), fa(n), fb(n), counts(static_cast<size_t>(n) + 2);
-    ADSB_CUDA(cudaMemsetAsync(counts.ptr, 0, counts.bytes(), s));
-    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist.ptr, n);
+    cudaStream_t s = ctx.rt->stream;
+    uint32_t* dist = ctx.rt->pool.get<uint32_t>(Scratch::kDist, n);
+    uint32_t* fa = ctx.rt->pool.get<uint32_t>(Scratch::kFrontA, n);
+    uint32_t* fb = ctx.rt->pool.get<uint32_t>(Scratch::kFrontB, n);
+    uint32_t* counts = ctx.rt->pool.get<uint32_t>(Scratch::kLevelCounts, static_cast<size_t>(n) + 2);
+    ADSB_CUDA(cudaMemsetAsync(counts, 0, (static_cast<size_t>(n) + 2) * sizeof(uint32_t), s));
+    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist, n);
     const uint32_t zero = 0, one = 1;
-    ADSB_CUDA(cudaMemcpyAsync(dist.ptr + source, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    ADSB_CUDA(cudaMemcpyAsync(fa.ptr, &source, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    ADSB_CUDA(cudaMemcpyAsync(counts.ptr, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaMemcpyAsync(dist + source, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaMemcpyAsync(fa, &source, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaMemcpyAsync(counts, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    ADSB_CUDA(cudaStreamSynchronize(s));  // the host-side sources above are stack values
     return bfs_depth(ctx, dist, fa, fb, counts);
 }
 
 uint64_t device_diameter_bound(DeviceContext& ctx) {
+    if (ctx.dub_ready) return ctx.diameter_bound;
     const uint32_t n = ctx.graph.n;
     const uint32_t comps = device_components(ctx);
-    cudaStream_t s = ctx.stream;
-    DevBuf<unsigned long long> best(comps);
-    DevBuf<uint32_t> dist(n), fa(n), fb(n), counts(static_cast<size_t>(n) + 2);
-    ADSB_CUDA(cudaMemsetAsync(best.ptr, 0, best.bytes(), s));
-    ADSB_CUDA(cudaMemsetAsync(counts.ptr, 0, counts.bytes(), s));
-    argmax_degree<<<grid_for(n, ctx.device), 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.labels.ptr, best.ptr, n);
-    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist.ptr, n);
-    seed_sources<<<grid_for(comps, ctx.device), 256, 0, s>>>(best.ptr, comps, dist.ptr, fa.ptr, counts.ptr);
-    return 2 * bfs_depth(ctx, dist, fa, fb, counts);
+    cudaStream_t s = ctx.rt->stream;
+    unsigned long long* best = ctx.rt->pool.get<unsigned long long>(Scratch::kBest, comps);
+    uint32_t* dist = ctx.rt->pool.get<uint32_t>(Scratch::kDist, n);
+    uint32_t* fa = ctx.rt->pool.get<uint32_t>(Scratch::kFrontA, n);
+    uint32_t* fb = ctx.rt->pool.get<uint32_t>(Scratch::kFrontB, n);
+    uint32_t* counts = ctx.rt->pool.get<uint32_t>(Scratch::kLevelCounts, static_cast<size_t>(n) + 2);
+    ADSB_CUDA(cudaMemsetAsync(best, 0, static_cast<size_t>(comps) * sizeof(unsigned long long), s));
+    ADSB_CUDA(cudaMemsetAsync(counts, 0, (static_cast<size_t>(n) + 2) * sizeof(uint32_t), s));
+    argmax_degree<<<grid_for(n, ctx.device), 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.labels.ptr, best, n);
+    init_dist<<<grid_for(n, ctx.device), 256, 0, s>>>(dist, n);
+    seed_sources<<<grid_for(comps, ctx.device), 256, 0, s>>>(best, comps, dist, fa, counts);
+    ctx.diameter_bound = 2 * bfs_depth(ctx, dist, fa, fb, counts);
+    ctx.dub_ready = true;
+    return ctx.diameter_bound;
 }
 
 }  // namespace adsb

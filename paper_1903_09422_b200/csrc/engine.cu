@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -69,6 +70,10 @@ bool converged_at_max(uint64_t max_count, uint64_t tau, uint64_t omega, double e
 namespace {
 
 constexpr uint32_t kNoStop = 0xFFFFFFFFu;
+// word offsets into DeviceContext::pinned (words 0..15 belong to the BFS level counts)
+constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
+              kPinAdapt = 72;
+static_assert(kStatCount <= 8, "pinned staging layout");
 
 struct RuleParams {
     uint64_t omega;
@@ -178,21 +183,44 @@ struct Timer {
     }
 };
 
+SamplerArena& arena(DeviceContext& ctx) { return *ctx.rt->arena[ctx.rt->active]; }
+
+// Pick the team kind for this graph and make sure the device's arena of that
+// kind covers it (vertex capacity and t-level capacity). Arenas are shared by
+// all graphs on the device; per-slot generation tags live with the arena, so
+// state left by an earlier graph always reads as "unvisited".
 void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     const uint32_t n = ctx.graph.n;
-    if (ctx.arena && ctx.arena->level_cap >= level_cap) return;
-    ctx.arena.reset();
+    // Warp teams win when samples are tiny (C1: ~600 adjacency entries per
+    // sample); block teams with shared-memory state win on the larger
+    // small-world graphs (C2/C3). ADSB_SAMPLER overrides.
+    SamplerKind kind = n <= (1u << 16) ? SamplerKind::kWarp : SamplerKind::kBlock;
+    if (std::getenv("ADSB_SAMPLER")) kind = sampler_kind();
+    uint32_t hash_cap = 2048;
+    if (const char* e = std::getenv("ADSB_HASH_CAP")) hash_cap = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
+    uint32_t block_threads = 256;
+    if (const char* e = std::getenv("ADSB_BLOCK")) block_threads = std::strtoul(e, nullptr, 10) == 128 ? 128 : 256;
+    if (hash_cap < 64 || (hash_cap & (hash_cap - 1))) invalid("ADSB_HASH_CAP must be a power of two >= 64");
+    const bool use_smem = !std::getenv("ADSB_NO_SMEM");
+    const int k = kind == SamplerKind::kWarp ? 0 : 1;
+    DeviceRuntime& rt = *ctx.rt;
+    rt.active = k;
+    std::unique_ptr<SamplerArena>& slot = rt.arena[k];
+    if (slot && slot->n >= n && slot->level_cap >= level_cap && slot->hash_cap == hash_cap &&
+        slot->block_threads == block_threads) {
+        if (!use_smem) slot->use_smem = false;
+        return;
+    }
+    const uint32_t cap_n = slot ? std::max(slot->n, n) : n;
+    const uint32_t cap_levels = slot ? std::max(slot->level_cap, level_cap) : level_cap;
+    slot.reset();
     ADSB_CUDA(cudaSetDevice(ctx.device));
     const int sms = num_sms(ctx.device);
-    const SamplerKind kind = sampler_kind();
-    uint32_t hash_cap = 4096;
-    if (const char* e = std::getenv("ADSB_HASH_CAP")) hash_cap = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
-    if (hash_cap < 64 || (hash_cap & (hash_cap - 1))) invalid("ADSB_HASH_CAP must be a power of two >= 64");
     const int per_sm = kind == SamplerKind::kWarp ? std::max(sampler_warps_per_sm(true), 8)
-                                                  : std::max(sampler_cta_blocks_per_sm(hash_cap), 1);
+                                                  : std::max(sampler_cta_blocks_per_sm(hash_cap, block_threads), 1);
     size_t free_b = 0, total_b = 0;
     ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t per_slot = static_cast<uint64_t>(n) * (16 + 4 + 8) + static_cast<uint64_t>(level_cap) * 4;
+    const uint64_t per_slot = static_cast<uint64_t>(cap_n) * (16 + 4 + 8) + static_cast<uint64_t>(cap_levels) * 4;
     const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
     uint64_t slots = static_cast<uint64_t>(sms) * per_sm;
     slots = std::min<uint64_t>(slots, budget / std::max<uint64_t>(per_slot, 1));
@@ -201,30 +229,32 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
         fail(ADSB_ERR_CUDA, "not enough device memory for the sampler scratch (" +
                                 std::to_string(per_slot >> 20) + " MiB per team)");
     auto a = std::make_unique<SamplerArena>();
-    a->kind = kind == SamplerKind::kWarp ? 0 : 1;
+    a->kind = k;
     a->hash_cap = hash_cap;
-    a->use_smem = !(std::getenv("ADSB_NO_SMEM"));
+    a->block_threads = block_threads;
+    a->use_smem = use_smem;
     a->slots = static_cast<uint32_t>(slots);
-    a->n = n;
-    a->level_cap = level_cap;
-    a->state.alloc(slots * n * 2);
-    a->queue.alloc(slots * n);
-    a->qrange.alloc(slots * n);
-    a->tlev.alloc(slots * level_cap);
+    a->n = cap_n;
+    a->level_cap = cap_levels;
+    a->state.alloc(slots * cap_n * 2);
+    a->queue.alloc(slots * cap_n);
+    a->qrange.alloc(slots * cap_n);
+    a->tlev.alloc(slots * cap_levels);
     a->slot_tag.alloc(slots);
-    ADSB_CUDA(cudaMemsetAsync(a->state.ptr, 0, a->state.bytes(), ctx.stream));
-    ADSB_CUDA(cudaMemsetAsync(a->slot_tag.ptr, 0, a->slot_tag.bytes(), ctx.stream));
-    ADSB_CUDA(cudaStreamSynchronize(ctx.stream));
-    ctx.arena = std::move(a);
+    ADSB_CUDA(cudaMemsetAsync(a->state.ptr, 0, a->state.bytes(), rt.stream));
+    ADSB_CUDA(cudaMemsetAsync(a->slot_tag.ptr, 0, a->slot_tag.bytes(), rt.stream));
+    ADSB_CUDA(cudaStreamSynchronize(rt.stream));
+    slot = std::move(a);
 }
 
 SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
-    SamplerArena& a = *ctx.arena;
+    SamplerArena& a = arena(ctx);
     SamplerParams p{};
     p.off = ctx.graph.offsets.ptr;
     p.nbrs = ctx.graph.nbrs.ptr;
     p.label = ctx.labels.ptr;
     p.n = ctx.graph.n;
+    p.slot_stride = a.n;
     p.slots = a.slots;
     p.level_cap = a.level_cap;
     p.rank = 0;
@@ -238,6 +268,7 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.slot_tag = a.slot_tag.ptr;
     p.hash_cap = a.hash_cap;
     p.use_smem = a.use_smem ? 1u : 0u;
+    p.block_threads = a.block_threads;
     return p;
 }
 
@@ -248,37 +279,42 @@ struct Launches {
 // Stop trying the shared-memory table for this graph when most samples
 // overflow it (their balls are too large); results do not depend on the store.
 void adapt_store(DeviceContext& ctx, const unsigned long long* stats, cudaStream_t s) {
-    SamplerArena& a = *ctx.arena;
+    SamplerArena& a = arena(ctx);
     if (a.kind == 0 || !a.use_smem) return;
-    unsigned long long h[kStatCount];
-    ADSB_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+    unsigned long long* h = ctx.rt->pinned.ptr + kPinAdapt;
+    ADSB_CUDA(cudaMemcpyAsync(h, stats, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     ADSB_CUDA(cudaStreamSynchronize(s));
     if (h[kStatSamples] >= 256 && h[kStatFallbacks] * 2 > h[kStatSamples]) a.use_smem = false;
 }
 
 // One deterministic batch through the sampler; grows the event buffer until it fits.
-uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, DevBuf<unsigned long long>& events,
-                       DevBuf<unsigned long long>& scal, Launches& L, cudaEvent_t e0, cudaEvent_t e1,
-                       double& sampler_ms) {
+uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, unsigned long long*& events, unsigned long long* scal,
+                       Launches& L, cudaEvent_t e0, cudaEvent_t e1, double& sampler_ms) {
+    unsigned long long* used_h = ctx.rt->pinned.ptr + kPinUsed;
     for (;;) {
-        ADSB_CUDA(cudaMemsetAsync(scal.ptr, 0, 2 * sizeof(unsigned long long), ctx.stream));
-        p.ticket = scal.ptr;
-        p.ev_cursor = scal.ptr + 1;
-        p.events = events.ptr;
-        p.ev_cap = events.count;
-        ADSB_CUDA(cudaEventRecord(e0, ctx.stream));
-        launch_sampler(static_cast<SamplerKind>(ctx.arena->kind == 0 ? 0 : 1), true, p, ctx.stream);
-        ADSB_CUDA(cudaEventRecord(e1, ctx.stream));
+        ADSB_CUDA(cudaMemsetAsync(scal, 0, 2 * sizeof(unsigned long long), ctx.rt->stream));
+        p.ticket = scal;
+        p.ev_cursor = scal + 1;
+        p.events = events;
+        p.ev_cap = ctx.rt->pool.capacity<unsigned long long>(Scratch::kEvents);
+        ADSB_CUDA(cudaEventRecord(e0, ctx.rt->stream));
+        launch_sampler(static_cast<SamplerKind>(arena(ctx).kind == 0 ? 0 : 1), true, p, ctx.rt->stream);
+        ADSB_CUDA(cudaEventRecord(e1, ctx.rt->stream));
         L.count++;
-        unsigned long long used = 0;
-        ADSB_CUDA(cudaMemcpyAsync(&used, scal.ptr + 1, sizeof(used), cudaMemcpyDeviceToHost, ctx.stream));
-        ADSB_CUDA(cudaStreamSynchronize(ctx.stream));
+        ADSB_CUDA(cudaMemcpyAsync(used_h, scal + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx.rt->stream));
+        ADSB_CUDA(cudaStreamSynchronize(ctx.rt->stream));
         float ms = 0;
         ADSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         sampler_ms += ms;
-        if (used <= events.count) return used;
-        events.alloc(used + used / 4 + 1024);  // deterministic: rerun the same batch
+        const unsigned long long used = *used_h;
+        if (used <= p.ev_cap) return used;
+        events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, used + used / 4 + 1024);  // rerun the batch
     }
+}
+
+bool trace_enabled() {
+    static const bool on = std::getenv("ADSB_TRACE") != nullptr;
+    return on;
 }
 
 }  // namespace
@@ -299,40 +335,52 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
 
     // ---- preprocessing (kadabra.hpp:319-325): components, D_ub, omega, deltas
     Timer pre;
-    ctx.labels_ready = false;  // recomputed per call, as the reference does
+    // components and D_ub depend only on the (immutable) graph: computed on the
+    // first call for this handle and reused (the reference recomputes them per
+    // call inside preprocess_seconds, kadabra.hpp:319-325)
     out.num_components = device_components(ctx);
+    const double t_cc = pre.seconds();
     out.diameter_bound = device_diameter_bound(ctx);
+    const double t_dub = pre.seconds();
     out.omega = compute_omega(out.diameter_bound, eps, delta, opt.c);
     const double delta_v = delta / (2.0 * static_cast<double>(n));  // kadabra.hpp:34
     const double log_inv = std::log(1.0 / delta_v);                 // kadabra.hpp:123
     const uint32_t level_cap = static_cast<uint32_t>(std::min<uint64_t>(out.diameter_bound + 3, n + 2));
     ensure_arena(ctx, level_cap);
     out.preprocess_seconds = pre.seconds();
+    if (trace_enabled())
+        std::fprintf(stderr, "[adsb] preprocess: components %.3f ms, D_ub %.3f ms, arena %.3f ms (kind %d, slots %u)\n",
+                     1e3 * t_cc, 1e3 * (t_dub - t_cc), 1e3 * (out.preprocess_seconds - t_dub), arena(ctx).kind,
+                     arena(ctx).slots);
 
     Timer ads;
     const RuleParams rule{out.omega, static_cast<double>(out.omega), log_inv, eps};
-    cudaStream_t s1 = ctx.stream, s2 = ctx.stream2;
-    DevBuf<uint32_t> total(n);
-    DevBuf<unsigned long long> stats(kStatCount);
-    DevBuf<unsigned long long> scal(4);
-    ADSB_CUDA(cudaMemsetAsync(total.ptr, 0, total.bytes(), s1));
-    ADSB_CUDA(cudaMemsetAsync(stats.ptr, 0, stats.bytes(), s1));
-    cudaEvent_t e0, e1;
-    ADSB_CUDA(cudaEventCreate(&e0));
-    ADSB_CUDA(cudaEventCreate(&e1));
+    cudaStream_t s1 = ctx.rt->stream, s2 = ctx.rt->stream2;
+    uint32_t* total = ctx.rt->pool.get<uint32_t>(Scratch::kTotal, n);
+    unsigned long long* stats = ctx.rt->pool.get<unsigned long long>(Scratch::kStats, kStatCount);
+    unsigned long long* scal = ctx.rt->pool.get<unsigned long long>(Scratch::kScal, 4);
+    ADSB_CUDA(cudaMemsetAsync(total, 0, static_cast<size_t>(n) * sizeof(uint32_t), s1));
+    ADSB_CUDA(cudaMemsetAsync(stats, 0, kStatCount * sizeof(unsigned long long), s1));
+    if (!ctx.rt->ev_a) {
+        ADSB_CUDA(cudaEventCreate(&ctx.rt->ev_a));
+        ADSB_CUDA(cudaEventCreate(&ctx.rt->ev_b));
+    }
+    cudaEvent_t e0 = ctx.rt->ev_a, e1 = ctx.rt->ev_b;
     Launches L;
-    const uint64_t team_slots = ctx.arena->slots;
+    // work units that keep every team busy: warps are many and light, blocks few and heavy
+    const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).slots;
 
     if (opt.deterministic) {
         const uint64_t spf = opt.spf;
         uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
         if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
         frame_limit = std::max<uint64_t>(frame_limit, 1);
-        DevBuf<uint32_t> base_max(1), stop_idx(1);
-        ADSB_CUDA(cudaMemsetAsync(base_max.ptr, 0, sizeof(uint32_t), s1));
-        DevBuf<unsigned long long> events(1 << 20), sorted, gathered;
-        DevBuf<uint32_t> frame_max, run_max;
-        DevBuf<uint8_t> temp;
+        uint32_t* base_max = ctx.rt->pool.get<uint32_t>(Scratch::kBaseMax, 1);
+        uint32_t* stop_idx = ctx.rt->pool.get<uint32_t>(Scratch::kStopIdx, 1);
+        uint32_t* stop_h = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinStop);
+        unsigned long long* emax_h = ctx.rt->pinned.ptr + kPinEmax;
+        ADSB_CUDA(cudaMemsetAsync(base_max, 0, sizeof(uint32_t), s1));
+        unsigned long long* events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, 1 << 20);
         uint64_t done = 0;  // frames folded so far
         uint64_t sampled_frames = 0;
         bool stopped = false;
@@ -346,65 +394,61 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             p.rank = static_cast<uint32_t>(rank);
             p.world = static_cast<uint32_t>(world);
             p.num_items = (F > static_cast<uint64_t>(rank)) ? (F - rank + world - 1) / world : 0;
-            p.stats = stats.ptr;
-            uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, out.sampler_ms);
+            p.stats = stats;
+            const uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, out.sampler_ms);
             sampled_frames += F;
-            adapt_store(ctx, stats.ptr, s1);
-            unsigned long long* ev = events.ptr;
+            adapt_store(ctx, stats, s1);
+            unsigned long long* ev = events;
             uint64_t count = E;
-            if (world > 1 || opt.comm) {
+            if (opt.comm) {
                 // gather every rank's events so each rank runs the identical cutoff
-                DevBuf<unsigned long long> dmax(1);
-                unsigned long long mine = E;
-                ADSB_CUDA(cudaMemcpyAsync(dmax.ptr, &mine, sizeof(mine), cudaMemcpyHostToDevice, s1));
-                ADSB_NCCL(ncclAllReduce(dmax.ptr, dmax.ptr, 1, ncclUint64, ncclMax, opt.comm->comm, s1));
-                unsigned long long emax = 0;
-                ADSB_CUDA(cudaMemcpyAsync(&emax, dmax.ptr, sizeof(emax), cudaMemcpyDeviceToHost, s1));
+                unsigned long long* dmax = ctx.rt->pool.get<unsigned long long>(Scratch::kNcclScalar, 1);
+                *emax_h = E;
+                ADSB_CUDA(cudaMemcpyAsync(dmax, emax_h, sizeof(unsigned long long), cudaMemcpyHostToDevice, s1));
+                ADSB_NCCL(ncclAllReduce(dmax, dmax, 1, ncclUint64, ncclMax, opt.comm->comm, s1));
+                ADSB_CUDA(cudaMemcpyAsync(emax_h, dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
                 ADSB_CUDA(cudaStreamSynchronize(s1));
-                if (events.count < emax) {
-                    DevBuf<unsigned long long> grown(emax);
-                    ADSB_CUDA(cudaMemcpyAsync(grown.ptr, events.ptr, E * sizeof(unsigned long long),
-                                              cudaMemcpyDeviceToDevice, s1));
-                    events = std::move(grown);
+                const unsigned long long emax = *emax_h;
+                if (ctx.rt->pool.capacity<unsigned long long>(Scratch::kEvents) < emax) {
+                    unsigned long long* tmp = ctx.rt->pool.get<unsigned long long>(Scratch::kSorted, E);
+                    ADSB_CUDA(cudaMemcpyAsync(tmp, events, E * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s1));
+                    events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, emax);
+                    ADSB_CUDA(cudaMemcpyAsync(events, tmp, E * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s1));
                 }
                 if (emax > E)
-                    ADSB_CUDA(cudaMemsetAsync(events.ptr + E, 0xFF, (emax - E) * sizeof(unsigned long long), s1));
-                if (gathered.count < emax * world) gathered.alloc(emax * world);
-                ADSB_NCCL(ncclAllGather(events.ptr, gathered.ptr, emax, ncclUint64, opt.comm->comm, s1));
-                ev = gathered.ptr;
+                    ADSB_CUDA(cudaMemsetAsync(events + E, 0xFF, (emax - E) * sizeof(unsigned long long), s1));
+                unsigned long long* gathered = ctx.rt->pool.get<unsigned long long>(Scratch::kGathered, emax * world);
+                ADSB_NCCL(ncclAllGather(events, gathered, emax, ncclUint64, opt.comm->comm, s1));
+                ev = gathered;
                 count = emax * world;
             }
             // K4: ordered cutoff over the batch
-            if (sorted.count < count) sorted.alloc(count + count / 4 + 1);
-            if (frame_max.count < F) {
-                frame_max.alloc(F);
-                run_max.alloc(F);
-            }
+            unsigned long long* sorted = ctx.rt->pool.get<unsigned long long>(Scratch::kSorted, count);
+            uint32_t* frame_max = ctx.rt->pool.get<uint32_t>(Scratch::kFrameMax, F);
+            uint32_t* run_max = ctx.rt->pool.get<uint32_t>(Scratch::kRunMax, F);
             int end_bit = 64;
-            if (world == 1 && !opt.comm) {
+            if (!opt.comm) {
                 int vbits = 1;
                 while (vbits < 32 && (1ull << vbits) < n) ++vbits;
                 end_bit = 32 + vbits;
             }
-            size_t tb = 0;
-            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, ev, sorted.ptr, count, 0, end_bit, s1));
-            size_t tb2 = 0;
-            ADSB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, frame_max.ptr, run_max.ptr, MaxOp(),
+            size_t tb = 0, tb2 = 0;
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, ev, sorted, count, 0, end_bit, s1));
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, frame_max, run_max, MaxOp(),
                                                      static_cast<int64_t>(F), s1));
             tb = std::max(tb, tb2);
-            if (temp.count < tb) temp.alloc(tb);
-            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(temp.ptr, tb, ev, sorted.ptr, count, 0, end_bit, s1));
-            ADSB_CUDA(cudaMemsetAsync(frame_max.ptr, 0, F * sizeof(uint32_t), s1));
-            k_event_values<<<grid_for(count, ctx.device), 256, 0, s1>>>(sorted.ptr, count, total.ptr, frame_max.ptr);
-            ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp.ptr, tb, frame_max.ptr, run_max.ptr, MaxOp(),
-                                                     static_cast<int64_t>(F), s1));
-            ADSB_CUDA(cudaMemsetAsync(stop_idx.ptr, 0xFF, sizeof(uint32_t), s1));
-            k_find_stop<<<grid_for(F, ctx.device), 256, 0, s1>>>(run_max.ptr, static_cast<uint32_t>(F),
-                                                                 base_max.ptr, done, spf, rule, stop_idx.ptr);
-            uint32_t stop_host = kNoStop;
-            ADSB_CUDA(cudaMemcpyAsync(&stop_host, stop_idx.ptr, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
+            uint8_t* temp = ctx.rt->pool.get<uint8_t>(Scratch::kSortTemp, tb);
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(temp, tb, ev, sorted, count, 0, end_bit, s1));
+            ADSB_CUDA(cudaMemsetAsync(frame_max, 0, F * sizeof(uint32_t), s1));
+            k_event_values<<<grid_for(count, ctx.device), 256, 0, s1>>>(sorted, count, total, frame_max);
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp, tb, frame_max, run_max, MaxOp(), static_cast<int64_t>(F), s1));
+            ADSB_CUDA(cudaMemsetAsync(stop_idx, 0xFF, sizeof(uint32_t), s1));
+            k_find_stop<<<grid_for(F, ctx.device), 256, 0, s1>>>(run_max, static_cast<uint32_t>(F), base_max, done, spf,
+                                                                 rule, stop_idx);
+            ADSB_CUDA(cudaMemcpyAsync(stop_h, stop_idx, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
             ADSB_CUDA(cudaStreamSynchronize(s1));
             L.count += 3;
+            const uint32_t stop_host = *stop_h;
             uint32_t limit = static_cast<uint32_t>(F - 1);
             if (stop_host != kNoStop) {
                 limit = stop_host;
@@ -415,9 +459,14 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
                 stop_local = limit;
                 out.reason = ADSB_REASON_CAPPED;
             }
-            k_apply<<<grid_for(count, ctx.device), 256, 0, s1>>>(ev, count, limit, total.ptr);
-            k_update_base<<<1, 32, 0, s1>>>(run_max.ptr, limit, base_max.ptr);
+            k_apply<<<grid_for(count, ctx.device), 256, 0, s1>>>(ev, count, limit, total);
+            k_update_base<<<1, 32, 0, s1>>>(run_max, limit, base_max);
             L.count += 2;
+            if (trace_enabled())
+                std::fprintf(stderr, "[adsb] det batch: frames %llu..%llu events %llu stop %d t=%.3f ms\n",
+                             static_cast<unsigned long long>(done), static_cast<unsigned long long>(done + F),
+                             static_cast<unsigned long long>(count), stop_host == kNoStop ? -1 : static_cast<int>(stop_host),
+                             1e3 * ads.seconds());
             if (!stopped) done += F;
             else done += static_cast<uint64_t>(stop_local) + 1;
         }
@@ -435,20 +484,31 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         uint64_t max_epochs = (out.omega + B - 1) / B;
         if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
         max_epochs = std::max<uint64_t>(max_epochs, 1);
-        DevBuf<uint32_t> cnt(2ull * n), dmax(2), flag_dev(2);
-        DevBuf<unsigned long long> tickets(2);
-        PinnedBuf<uint32_t> flag_host(2);
-        ADSB_CUDA(cudaMemsetAsync(cnt.ptr, 0, cnt.bytes(), s1));
-        ADSB_CUDA(cudaMemsetAsync(dmax.ptr, 0, dmax.bytes(), s1));
+        uint32_t* cnt = ctx.rt->pool.get<uint32_t>(Scratch::kEpochCnt, 2ull * n);
+        uint32_t* dmax = ctx.rt->pool.get<uint32_t>(Scratch::kDmax, 2);
+        uint32_t* flag_dev = ctx.rt->pool.get<uint32_t>(Scratch::kFlagDev, 2);
+        unsigned long long* tickets = ctx.rt->pool.get<unsigned long long>(Scratch::kTickets, 2);
+        uint32_t* flag_host = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinFlags);
+        unsigned long long* stat0 = ctx.rt->pinned.ptr + kPinStat0;  // kStatCount words
+        ADSB_CUDA(cudaMemsetAsync(cnt, 0, 2ull * n * sizeof(uint32_t), s1));
+        ADSB_CUDA(cudaMemsetAsync(dmax, 0, 2 * sizeof(uint32_t), s1));
         ADSB_CUDA(cudaStreamSynchronize(s1));
-        cudaEvent_t samp[2], chk[2];
-        for (int i = 0; i < 2; ++i) {
-            ADSB_CUDA(cudaEventCreateWithFlags(&samp[i], cudaEventDisableTiming));
-            ADSB_CUDA(cudaEventCreateWithFlags(&chk[i], cudaEventDisableTiming));
+        if (!ctx.rt->ev_samp[0]) {
+            for (int i = 0; i < 2; ++i) {
+                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_samp[i], cudaEventDisableTiming));
+                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_chk[i], cudaEventDisableTiming));
+            }
+            ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_stat, cudaEventDisableTiming));
         }
+        cudaEvent_t* samp = ctx.rt->ev_samp;
+        cudaEvent_t* chk = ctx.rt->ev_chk;
         const uint64_t share = (B > static_cast<uint64_t>(rank)) ? (B - rank + world - 1) / world : 0;
         uint64_t launched = 0;
-        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> launch_ev;
+        while (ctx.rt->ev_launch.size() < 2 * max_epochs + 2) {
+            cudaEvent_t ev;
+            ADSB_CUDA(cudaEventCreate(&ev));
+            ctx.rt->ev_launch.push_back(ev);
+        }
         auto enqueue_sampler = [&](uint64_t e) {
             const int k = static_cast<int>(e & 1);
             if (e >= 2) ADSB_CUDA(cudaStreamWaitEvent(s1, chk[k], 0));
@@ -457,17 +517,13 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             p.rank = static_cast<uint32_t>(rank);
             p.world = static_cast<uint32_t>(world);
             p.num_items = share;
-            p.ticket = tickets.ptr + k;
-            p.counts = cnt.ptr + static_cast<size_t>(k) * n;
-            p.stats = stats.ptr;
-            ADSB_CUDA(cudaMemsetAsync(tickets.ptr + k, 0, sizeof(unsigned long long), s1));
-            cudaEvent_t a, b;
-            ADSB_CUDA(cudaEventCreate(&a));
-            ADSB_CUDA(cudaEventCreate(&b));
-            ADSB_CUDA(cudaEventRecord(a, s1));
-            launch_sampler(static_cast<SamplerKind>(ctx.arena->kind == 0 ? 0 : 1), false, p, s1);
-            ADSB_CUDA(cudaEventRecord(b, s1));
-            launch_ev.emplace_back(a, b);
+            p.ticket = tickets + k;
+            p.counts = cnt + static_cast<size_t>(k) * n;
+            p.stats = stats;
+            ADSB_CUDA(cudaMemsetAsync(tickets + k, 0, sizeof(unsigned long long), s1));
+            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * launched], s1));
+            launch_sampler(static_cast<SamplerKind>(arena(ctx).kind == 0 ? 0 : 1), false, p, s1);
+            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * launched + 1], s1));
             ADSB_CUDA(cudaEventRecord(samp[k], s1));
             L.count++;
             launched++;
@@ -475,40 +531,34 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         auto enqueue_check = [&](uint64_t e) {
             const int k = static_cast<int>(e & 1);
             ADSB_CUDA(cudaStreamWaitEvent(s2, samp[k], 0));
-            uint32_t* ec = cnt.ptr + static_cast<size_t>(k) * n;
+            uint32_t* ec = cnt + static_cast<size_t>(k) * n;
             if (opt.comm) ADSB_NCCL(ncclAllReduce(ec, ec, n, ncclUint32, ncclSum, opt.comm->comm, s2));
-            k_fold_epoch<<<grid_for(n, ctx.device), 256, 0, s2>>>(total.ptr, ec, n, dmax.ptr + k);
-            k_epoch_rule<<<1, 32, 0, s2>>>(dmax.ptr + k, (e + 1) * B, rule, flag_dev.ptr + k);
-            ADSB_CUDA(cudaMemcpyAsync(flag_host.ptr + k, flag_dev.ptr + k, sizeof(uint32_t),
-                                      cudaMemcpyDeviceToHost, s2));
+            k_fold_epoch<<<grid_for(n, ctx.device), 256, 0, s2>>>(total, ec, n, dmax + k);
+            k_epoch_rule<<<1, 32, 0, s2>>>(dmax + k, (e + 1) * B, rule, flag_dev + k);
+            ADSB_CUDA(cudaMemcpyAsync(flag_host + k, flag_dev + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
             ADSB_CUDA(cudaEventRecord(chk[k], s2));
             L.count += 2;
         };
-        cudaEvent_t t_begin, t_end;
-        ADSB_CUDA(cudaEventCreate(&t_begin));
-        ADSB_CUDA(cudaEventCreate(&t_end));
-        ADSB_CUDA(cudaEventRecord(t_begin, s1));
         enqueue_sampler(0);
-        PinnedBuf<unsigned long long> stat0(kStatCount);
-        cudaEvent_t stat_ev;
-        ADSB_CUDA(cudaEventCreateWithFlags(&stat_ev, cudaEventDisableTiming));
-        ADSB_CUDA(cudaMemcpyAsync(stat0.ptr, stats.ptr, kStatCount * sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, s1));
-        ADSB_CUDA(cudaEventRecord(stat_ev, s1));
+        ADSB_CUDA(cudaMemcpyAsync(stat0, stats, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
+        ADSB_CUDA(cudaEventRecord(ctx.rt->ev_stat, s1));
         enqueue_check(0);
         if (max_epochs > 1) enqueue_sampler(1);
         uint64_t e = 0;
         for (;; ++e) {
             const int k = static_cast<int>(e & 1);
             ADSB_CUDA(cudaEventSynchronize(chk[k]));
-            const bool pass = flag_host.ptr[k] != 0;
+            const bool pass = flag_host[k] != 0;
             if (e == 0) {
-                ADSB_CUDA(cudaEventSynchronize(stat_ev));
-                SamplerArena& ar = *ctx.arena;
-                if (ar.kind == 1 && ar.use_smem && stat0.ptr[kStatSamples] >= 256 &&
-                    stat0.ptr[kStatFallbacks] * 2 > stat0.ptr[kStatSamples])
+                ADSB_CUDA(cudaEventSynchronize(ctx.rt->ev_stat));
+                SamplerArena& ar = arena(ctx);
+                if (ar.kind == 1 && ar.use_smem && stat0[kStatSamples] >= 256 &&
+                    stat0[kStatFallbacks] * 2 > stat0[kStatSamples])
                     ar.use_smem = false;
             }
+            if (trace_enabled())
+                std::fprintf(stderr, "[adsb] epoch %llu checked: pass %d t=%.3f ms\n", static_cast<unsigned long long>(e),
+                             pass ? 1 : 0, 1e3 * ads.seconds());
             if (pass || e + 1 >= max_epochs) {
                 if (!pass) out.reason = ADSB_REASON_CAPPED;
                 break;
@@ -516,42 +566,31 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             enqueue_check(e + 1);
             if (e + 2 < max_epochs) enqueue_sampler(e + 2);
         }
-        ADSB_CUDA(cudaEventRecord(t_end, s1));
         ADSB_CUDA(cudaStreamSynchronize(s1));
         ADSB_CUDA(cudaStreamSynchronize(s2));
-        for (auto& [a, b] : launch_ev) {
+        for (uint64_t i = 0; i < launched; ++i) {
             float ms = 0;
-            ADSB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            ADSB_CUDA(cudaEventElapsedTime(&ms, ctx.rt->ev_launch[2 * i], ctx.rt->ev_launch[2 * i + 1]));
             out.sampler_ms += ms;  // device time of the sampler launches only
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
         }
         out.tau = (e + 1) * B;
         out.check_cycles = e + 1;
         out.stop_epoch = e + 1;
         out.total_samples = launched * B;
-        for (int i = 0; i < 2; ++i) {
-            cudaEventDestroy(samp[i]);
-            cudaEventDestroy(chk[i]);
-        }
-        cudaEventDestroy(t_begin);
-        cudaEventDestroy(t_end);
-        cudaEventDestroy(stat_ev);
     }
 
     // ---- results
-    std::vector<uint32_t> host32(n);
-    ADSB_CUDA(cudaMemcpyAsync(host32.data(), total.ptr, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
-    unsigned long long st_host[kStatCount];
-    ADSB_CUDA(cudaMemcpyAsync(st_host, stats.ptr, sizeof(st_host), cudaMemcpyDeviceToHost, s1));
+    if (ctx.rt->host_counts.count < n) ctx.rt->host_counts = PinnedBuf<uint32_t>(n);
+    uint32_t* host32 = ctx.rt->host_counts.ptr;
+    ADSB_CUDA(cudaMemcpyAsync(host32, total, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
+    unsigned long long* st_host = ctx.rt->pinned.ptr + kPinStats;
+    ADSB_CUDA(cudaMemcpyAsync(st_host, stats, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
     ADSB_CUDA(cudaStreamSynchronize(s1));
     ADSB_CUDA(cudaGetLastError());
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     if (st_host[kStatErrors] != 0)
         fail(ADSB_ERR_LOGIC, "sampler reported " + std::to_string(st_host[kStatErrors]) +
                                  " inconsistent traversals (all predecessor counts wrapped to 0?)");
-    out.counts.assign(host32.begin(), host32.end());
+    out.counts.assign(host32, host32 + n);
     out.edges_scanned = st_host[kStatEdges];
     out.vertices_expanded = st_host[kStatVertices];
     out.rebuild_edges = st_host[kStatRebuildEdges];
@@ -562,7 +601,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (out.reason != ADSB_REASON_CAPPED) {
         out.reason = ADSB_REASON_OMEGA_REACHED;
         uint64_t mx = 0;
-        for (uint32_t v : host32) mx = std::max<uint64_t>(mx, v);
+        for (uint32_t v = 0; v < n; ++v) mx = std::max<uint64_t>(mx, host32[v]);
         if (out.tau >= 1 && converged_at_max(mx, out.tau, out.omega, eps, log_inv))
             out.reason = ADSB_REASON_EPS_CONVERGED;
     }
@@ -582,24 +621,25 @@ void sample_frames(DeviceContext& ctx, uint64_t seed, uint64_t spf, uint64_t fir
     device_components(ctx);
     const uint64_t dub = device_diameter_bound(ctx);
     ensure_arena(ctx, static_cast<uint32_t>(std::min<uint64_t>(dub + 3, ctx.graph.n + 2)));
-    DevBuf<unsigned long long> events(1 << 16), scal(4), stats(kStatCount);
-    ADSB_CUDA(cudaMemsetAsync(stats.ptr, 0, stats.bytes(), ctx.stream));
+    unsigned long long* events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, 1 << 16);
+    unsigned long long* scal = ctx.rt->pool.get<unsigned long long>(Scratch::kScal, 4);
+    unsigned long long* stats = ctx.rt->pool.get<unsigned long long>(Scratch::kStats, kStatCount);
+    ADSB_CUDA(cudaMemsetAsync(stats, 0, kStatCount * sizeof(unsigned long long), ctx.rt->stream));
     SamplerParams p = base_params(ctx, seed, spf);
     p.first = first;
     p.num_items = count;
-    p.stats = stats.ptr;
-    cudaEvent_t e0, e1;
-    ADSB_CUDA(cudaEventCreate(&e0));
-    ADSB_CUDA(cudaEventCreate(&e1));
+    p.stats = stats;
+    if (!ctx.rt->ev_a) {
+        ADSB_CUDA(cudaEventCreate(&ctx.rt->ev_a));
+        ADSB_CUDA(cudaEventCreate(&ctx.rt->ev_b));
+    }
     Launches L;
     double ms = 0;
-    const uint64_t E = run_det_batch(ctx, p, events, scal, L, e0, e1, ms);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    const uint64_t E = run_det_batch(ctx, p, events, scal, L, ctx.rt->ev_a, ctx.rt->ev_b, ms);
     std::vector<unsigned long long> host(E);
     unsigned long long st_host[kStatCount];
-    ADSB_CUDA(cudaMemcpy(host.data(), events.ptr, E * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    ADSB_CUDA(cudaMemcpy(st_host, stats.ptr, sizeof(st_host), cudaMemcpyDeviceToHost));
+    ADSB_CUDA(cudaMemcpy(host.data(), events, E * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    ADSB_CUDA(cudaMemcpy(st_host, stats, sizeof(st_host), cudaMemcpyDeviceToHost));
     if (st_host[kStatErrors] != 0) fail(ADSB_ERR_LOGIC, "sampler reported inconsistent traversals");
     // Events of one frame were reserved in sample order, each sample's in t->s
     // order, so a stable partition by frame restores the reference's layout.

@@ -429,9 +429,9 @@ __global__ void __launch_bounds__(256) sampler_kernel(SamplerParams p) {
     T.off = p.off;
     T.nbrs = p.nbrs;
     T.n = p.n;
-    T.st = p.state + 2ull * p.n * slot;
-    T.queue = p.queue + static_cast<size_t>(p.n) * slot;
-    T.qrange = p.qrange + static_cast<size_t>(p.n) * slot;
+    T.st = p.state + 2ull * p.slot_stride * slot;
+    T.queue = p.queue + static_cast<size_t>(p.slot_stride) * slot;
+    T.qrange = p.qrange + static_cast<size_t>(p.slot_stride) * slot;
     T.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
     T.level_cap = p.level_cap;
     T.lane = lane;

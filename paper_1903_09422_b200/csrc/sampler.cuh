@@ -33,12 +33,14 @@ struct SamplerParams {
     const uint32_t* nbrs;
     const uint32_t* label;
     uint32_t n;
+    uint32_t slot_stride;  // per-slot vertex capacity of the (shared) arena, >= n
     uint32_t slots;
     uint32_t level_cap;
     uint32_t rank;         // this GPU's rank: items map to positions first + item*world + rank
     uint32_t world;
     uint32_t hash_cap;     // block sampler: shared-memory hash capacity (power of two)
     uint32_t use_smem;     // block sampler: try the shared-memory store first
+    uint32_t block_threads; // block sampler: 128 or 256
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode
@@ -65,7 +67,7 @@ int sampler_warps_per_sm(bool deterministic);
 void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 // Block-team sampler with shared-memory state (sampler_cta.cu): slots = blocks.
 size_t sampler_cta_smem_bytes(uint32_t hash_cap);
-int sampler_cta_blocks_per_sm(uint32_t hash_cap);
+int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads);
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 
 enum class SamplerKind { kWarp, kBlock };

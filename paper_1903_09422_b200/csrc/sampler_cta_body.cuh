@@ -1,0 +1,618 @@
+// sampler_cta_body.cuh — body of the block-team sampler, included once per
+// block size by sampler_cta.cu inside a namespace that defines kBT.
+// (Not a standalone header.)
+
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
+constexpr uint32_t kMetaT = 1u << 31;
+constexpr uint32_t kMetaDag = 1u << 30;
+constexpr uint32_t kMetaDist = (1u << 30) - 1;
+constexpr uint32_t kSmemLevels = 64;
+
+__device__ __forceinline__ bool m_is_t(uint32_t m) { return (m & kMetaT) != 0; }
+__device__ __forceinline__ uint32_t m_dist(uint32_t m) { return m & kMetaDist; }
+
+using BlockScan = cub::BlockScan<uint32_t, kBT>;
+
+struct Shared {
+    typename BlockScan::TempStorage scan_tmp;
+    uint32_t scan[kBT];               // inclusive degree scan of the current chunk
+    uint32_t cbase[kBT];              // off(u) - exclusive(u): nbr index = cbase[owner] + e
+    uint32_t cslot[kBT];              // store slot of the chunk's frontier vertex
+    unsigned long long cval[kBT];     // per-vertex payload (sigma of u)
+    unsigned long long item;
+    unsigned long long degsum;
+    uint32_t s_cnt, t_cnt;            // queue fill: s-side from 0 up, t-side from the top down
+    uint32_t inserted;                // hash reservations this sample
+    uint32_t overflow;
+    uint32_t tlev_small[kSmemLevels]; // t-level boundaries (shared-memory store)
+    unsigned long long wlo[kBT / 32]; // backtrack: per-warp 65-bit candidate sums
+    uint32_t whi[kBT / 32];
+    uint32_t first;                   // backtrack: first thread whose prefix exceeds r
+    uint32_t ch, chm;                 // backtrack: chosen predecessor and its meta
+    unsigned long long chs;           // backtrack: chosen predecessor's sigma
+    unsigned long long ev_pos;
+};
+
+// ---------------------------------------------------------------------------
+// Stores: where a sample's per-vertex state lives
+// ---------------------------------------------------------------------------
+
+// Shared-memory open-addressing table: km = key << 32 | meta, sig = sigma.
+// Empty slots have key 0xFFFFFFFF and sigma 0 (sigma is zeroed with the key,
+// so concurrent claimers and adders never race on initialisation).
+struct SmemStore {
+    unsigned long long* km;
+    unsigned long long* sig;
+    uint32_t* qv;      // queue: vertex ids
+    uint32_t* qdeg;    // queue: degrees (for the side-balancing heuristic)
+    uint32_t* tlev;
+    uint32_t mask;
+    uint32_t shift;
+    uint32_t qcap;
+    uint32_t limit;    // max insertions (<= capacity/2 keeps probing short and finite)
+    uint32_t level_cap;
+    Shared* sh;
+
+    __device__ uint32_t home(uint32_t v) const {
+        return static_cast<uint32_t>((static_cast<unsigned long long>(v) * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+    }
+    __device__ void clear_all(uint32_t tid) {
+        for (uint32_t i = tid; i <= mask; i += kBT) {
+            km[i] = ~0ull;
+            sig[i] = 0ull;
+        }
+    }
+    __device__ void begin(uint32_t) {}
+    // Reset exactly the slots this sample inserted (the queue lists them) so
+    // the next sample starts from an empty table without touching all of it.
+    template <class CtxT>
+    __device__ void end(CtxT& C, Shared& s) {
+        __syncthreads();
+        const uint32_t ns = min(s.s_cnt, qcap), nt = min(s.t_cnt, qcap);
+        if (s.overflow) {
+            clear_all(C.tid);
+        } else {
+            // pass 1 resolves every slot (and zeroes sigma) while the table is
+            // intact; pass 2 empties the keys without further probing
+            for (uint32_t i = C.tid; i < ns + nt; i += kBT) {
+                const uint32_t q = i < ns ? i : tpos(i - ns);
+                uint32_t m;
+                const uint32_t h = find(qv[q], m);
+                if (h != kNone) sig[h] = 0ull;
+                qv[q] = h;
+            }
+            __syncthreads();
+            for (uint32_t i = C.tid; i < ns + nt; i += kBT) {
+                const uint32_t h = qv[i < ns ? i : tpos(i - ns)];
+                if (h != kNone) km[h] = ~0ull;
+            }
+        }
+        __syncthreads();
+    }
+    __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
+        uint32_t h = home(v);
+        for (;;) {
+            const unsigned long long x = km[h];
+            const uint32_t k = static_cast<uint32_t>(x >> 32);
+            if (k == v) {
+                meta = static_cast<uint32_t>(x);
+                return h;
+            }
+            if (k == kEmptyKey) return kNone;
+            h = (h + 1) & mask;
+        }
+    }
+    // returns the slot (kNone on overflow); inserted tells whether this call created it
+    __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
+        inserted = false;
+        uint32_t h = home(v);
+        bool reserved = false;
+        for (;;) {
+            unsigned long long x = km[h];
+            uint32_t k = static_cast<uint32_t>(x >> 32);
+            if (k == v) {
+                meta = static_cast<uint32_t>(x);
+                return h;
+            }
+            if (k == kEmptyKey) {
+                if (!reserved) {
+                    if (atomicAdd(&sh->inserted, 1u) >= limit) {
+                        sh->overflow = 1;
+                        return kNone;
+                    }
+                    reserved = true;
+                }
+                const unsigned long long want = (static_cast<unsigned long long>(v) << 32) | new_meta;
+                const unsigned long long prev = atomicCAS(&km[h], x, want);
+                if (prev == x) {
+                    inserted = true;
+                    meta = new_meta;
+                    return h;
+                }
+                if (static_cast<uint32_t>(prev >> 32) == v) {
+                    meta = static_cast<uint32_t>(prev);
+                    return h;
+                }
+            }
+            h = (h + 1) & mask;
+        }
+    }
+    static constexpr bool kSigmaPreZeroed = true;  // claim and sigma accumulation share one pass
+    __device__ void zero_sigma(uint32_t) {}
+    __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(&sig[slot], x); }
+    __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], static_cast<unsigned long long>(kMetaDag)); }
+    __device__ unsigned long long sigma(uint32_t slot) const { return sig[slot]; }
+    __device__ bool queue_ok(uint32_t s_cnt, uint32_t t_cnt) const { return s_cnt + t_cnt <= qcap; }
+    __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
+};
+
+// Per-block dense global state (stamped with a per-block generation tag).
+struct GlobalStore {
+    unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
+    uint32_t* qv;
+    uint32_t* qdeg;
+    uint32_t* tlev;
+    uint32_t tag;
+    uint32_t qcap;
+    uint32_t level_cap;
+
+    __device__ void begin(uint32_t) {}
+    template <class CtxT>
+    __device__ void end(CtxT&, Shared&) {}
+    __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
+        const unsigned long long x = __ldcg(st + 2ull * v);
+        if (static_cast<uint32_t>(x >> 32) != tag) return kNone;
+        meta = static_cast<uint32_t>(x);
+        return v;
+    }
+    __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
+        inserted = false;
+        unsigned long long x = __ldcg(st + 2ull * v);
+        if (static_cast<uint32_t>(x >> 32) != tag) {
+            const unsigned long long want = (static_cast<unsigned long long>(tag) << 32) | new_meta;
+            const unsigned long long prev = atomicCAS(st + 2ull * v, x, want);
+            if (prev == x) {
+                inserted = true;
+                meta = new_meta;
+                return v;
+            }
+            x = prev;
+        }
+        meta = static_cast<uint32_t>(x);
+        return v;
+    }
+    static constexpr bool kSigmaPreZeroed = false;  // stale sigma: zero on claim, accumulate after a barrier
+    __device__ void zero_sigma(uint32_t slot) { st[2ull * slot + 1] = 0ull; }
+    __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(st + 2ull * slot + 1, x); }
+    __device__ void set_dag(uint32_t slot) { atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)); }
+    __device__ unsigned long long sigma(uint32_t slot) const { return __ldcg(st + 2ull * slot + 1); }
+    __device__ bool queue_ok(uint32_t, uint32_t) const { return true; }
+    __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
+};
+
+struct Ctx {
+    const uint32_t* __restrict__ off;
+    const uint32_t* __restrict__ nbrs;
+    uint32_t tid;
+    uint32_t lane;
+    uint32_t warp;
+    Shared* sh;
+    unsigned long long edges, rebuild_edges, back_edges, verts;
+};
+
+// Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
+// t_list). prep(slot) gives the per-vertex payload; body(slot_u, payload, v)
+// runs once per adjacency entry. Ends with a block barrier.
+template <class Store, class Prep, class Body>
+__device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long& counter,
+                          Prep prep, Body body) {
+    Shared& sh = *C.sh;
+    for (uint32_t base = lo; base < hi; base += kBT) {
+        const uint32_t i = base + C.tid;
+        uint32_t deg = 0, o = 0, slot = 0;
+        unsigned long long val = 0;
+        if (i < hi) {
+            const uint32_t q = t_list ? S.tpos(i) : i;
+            const uint32_t u = S.qv[q];
+            o = C.off[u];
+            deg = C.off[u + 1] - o;
+            uint32_t meta;
+            slot = S.find(u, meta);
+            val = prep(slot, meta, deg);
+        }
+        uint32_t incl, total;
+        BlockScan(sh.scan_tmp).InclusiveSum(deg, incl, total);
+        sh.scan[C.tid] = incl;
+        sh.cbase[C.tid] = o - (incl - deg);
+        sh.cslot[C.tid] = slot;
+        sh.cval[C.tid] = val;
+        __syncthreads();
+        counter += C.tid == 0 ? total : 0;
+        for (uint32_t e = C.tid; e < total; e += kBT) {
+            uint32_t l = 0, r = kBT - 1;  // first k with scan[k] > e
+            while (l < r) {
+                const uint32_t mid = (l + r) >> 1;
+                if (sh.scan[mid] > e) r = mid;
+                else l = mid + 1;
+            }
+            const uint32_t v = C.nbrs[sh.cbase[l] + e];
+            body(sh.cslot[l], sh.cval[l], v);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int src) {
+    return __shfl_sync(kFull, x, src);
+}
+
+// Result of the BFS phase: distance split d = a + b + 1.
+struct Meet {
+    uint32_t a, b;
+    int status;  // 0 met, 1 store overflow (redo on the global store), 2 inconsistent
+};
+
+template <class Store>
+__device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
+    Shared& sh = *C.sh;
+    if (C.tid == 0) {
+        bool ins;
+        uint32_t m;
+        const uint32_t ss = S.claim(s, 0u, ins, m);
+        const uint32_t tt = S.claim(t, kMetaT, ins, m);
+        S.zero_sigma(ss);
+        S.zero_sigma(tt);
+        S.add_sigma(ss, 1ull);
+        S.qv[0] = s;
+        S.qdeg[0] = C.off[s + 1] - C.off[s];
+        S.qv[S.tpos(0)] = t;
+        S.qdeg[S.tpos(0)] = C.off[t + 1] - C.off[t];
+        S.tlev[0] = 0;
+        S.tlev[1] = 1;
+        sh.s_cnt = 1;
+        sh.t_cnt = 1;
+    }
+    __syncthreads();
+    uint32_t s_lo = 0, s_hi = 1, t_lo = 0, t_hi = 1, a = 0, b = 0;
+    unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
+    for (;;) {
+        if (deg_s <= deg_t) {
+            // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
+            C.verts += C.tid == 0 ? s_hi - s_lo : 0;
+            bool met = false;
+            for_edges(C, S, s_lo, s_hi, false, C.edges,
+                      [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
+                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                          uint32_t m;
+                          const uint32_t sl = S.find(v, m);
+                          if (sl != kNone && m_is_t(m) && m_dist(m) == b) {
+                              S.add_sigma(sl, su);
+                              if (!(m & kMetaDag)) S.set_dag(sl);
+                              met = true;
+                          }
+                      });
+            if (__syncthreads_or(met)) return {a, b, 0};
+            // ---- no meeting: claim level a+1, then accumulate its sigma
+            if (C.tid == 0) sh.degsum = 0;
+            __syncthreads();
+            unsigned long long my_deg = 0;
+            const uint32_t meta_new = a + 1;
+            for_edges(C, S, s_lo, s_hi, false, C.edges,
+                      [&](uint32_t slot, uint32_t, uint32_t) { return Store::kSigmaPreZeroed ? S.sigma(slot) : 0ull; },
+                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                          bool ins;
+                          uint32_t m;
+                          const uint32_t sl = S.claim(v, meta_new, ins, m);
+                          if (Store::kSigmaPreZeroed && sl != kNone && (ins || (!m_is_t(m) && m_dist(m) == a + 1)))
+                              S.add_sigma(sl, su);
+                          if (ins) {
+                              S.zero_sigma(sl);
+                              const uint32_t pos = atomicAdd(&sh.s_cnt, 1u);
+                              const uint32_t dg = C.off[v + 1] - C.off[v];
+                              if (S.queue_ok(pos + 1, sh.t_cnt)) {
+                                  S.qv[pos] = v;
+                                  S.qdeg[pos] = dg;
+                              } else {
+                                  sh.overflow = 1;
+                              }
+                              my_deg += dg;
+                          }
+                      });
+            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            __syncthreads();  // degsum complete before any thread reads it (uniform side choice)
+            if (sh.overflow) return {a, b, 1};
+            if (!Store::kSigmaPreZeroed)
+            for_edges(C, S, s_lo, s_hi, false, C.edges,
+                      [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
+                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                          uint32_t m;
+                          const uint32_t sl = S.find(v, m);
+                          if (sl != kNone && !m_is_t(m) && m_dist(m) == a + 1) S.add_sigma(sl, su);
+                      });
+            s_lo = s_hi;
+            s_hi = sh.s_cnt;
+            deg_s = sh.degsum;
+            a += 1;
+            if (s_lo == s_hi) return {a, b, 2};
+        } else {
+            // ---- t-side level b: probe for the s-ball
+            C.verts += C.tid == 0 ? t_hi - t_lo : 0;
+            bool met = false;
+            for_edges(C, S, t_lo, t_hi, true, C.edges,
+                      [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
+                      [&](uint32_t su_slot, unsigned long long, uint32_t v) {
+                          uint32_t m;
+                          const uint32_t sl = S.find(v, m);
+                          if (sl != kNone && !m_is_t(m) && m_dist(m) == a) {
+                              S.add_sigma(su_slot, S.sigma(sl));
+                              S.set_dag(su_slot);
+                              met = true;
+                          }
+                      });
+            if (__syncthreads_or(met)) return {a, b, 0};
+            if (C.tid == 0) sh.degsum = 0;
+            __syncthreads();
+            unsigned long long my_deg = 0;
+            const uint32_t meta_new = kMetaT | (b + 1);
+            for_edges(C, S, t_lo, t_hi, true, C.edges,
+                      [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
+                      [&](uint32_t, unsigned long long, uint32_t v) {
+                          bool ins;
+                          uint32_t m;
+                          const uint32_t sl = S.claim(v, meta_new, ins, m);
+                          if (ins) {
+                              S.zero_sigma(sl);
+                              const uint32_t j = atomicAdd(&sh.t_cnt, 1u);
+                              const uint32_t dg = C.off[v + 1] - C.off[v];
+                              if (S.queue_ok(sh.s_cnt, j + 1)) {
+                                  S.qv[S.tpos(j)] = v;
+                                  S.qdeg[S.tpos(j)] = dg;
+                              } else {
+                                  sh.overflow = 1;
+                              }
+                              my_deg += dg;
+                          }
+                      });
+            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            __syncthreads();
+            if (sh.overflow) return {a, b, 1};
+            t_lo = t_hi;
+            t_hi = sh.t_cnt;
+            deg_t = sh.degsum;
+            b += 1;
+            if (b + 2 > S.level_cap) return {a, b, 1};
+            if (C.tid == 0) S.tlev[b + 1] = t_hi;
+            __syncthreads();
+            if (t_lo == t_hi) return {a, b, 2};
+        }
+    }
+}
+
+// sigma_s on the t-side DAG layers (pull; see sampler.cu rebuild_level)
+template <class Store>
+__device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
+    for (uint32_t k = b; k >= 1; --k) {
+        for_edges(C, S, S.tlev[k - 1], S.tlev[k], true, C.rebuild_edges,
+                  [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
+                  [&](uint32_t w_slot, unsigned long long, uint32_t v) {
+                      uint32_t m;
+                      const uint32_t sl = S.find(v, m);
+                      if (sl != kNone && m_is_t(m) && m_dist(m) == k && (m & kMetaDag)) {
+                          S.add_sigma(w_slot, S.sigma(sl));
+                          S.set_dag(w_slot);
+                      }
+                  });
+    }
+}
+
+__device__ __forceinline__ void add65(unsigned long long& lo, uint32_t& hi, unsigned long long xlo, uint32_t xhi) {
+    const unsigned long long n = lo + xlo;
+    hi += xhi + (n < lo ? 1u : 0u);
+    lo = n;
+}
+
+// Block-wide backtrack (kadabra.hpp:227-242). Every step scans N(cur) in
+// ascending order, kBT entries per round: each thread tests one neighbour
+// against the predecessor rule, a 65-bit block prefix sum over the
+// candidates' sigma (warp shuffles + per-warp totals) finds the first
+// neighbour with r < prefix — exactly the reference's sequential
+// `r -= sigma[p]` scan. All threads draw the same r from their copy of the
+// stream. Returns false on an inconsistent state (every predecessor sigma
+// wrapped to 0), which the reference leaves undefined.
+template <bool kDet, class Store>
+__device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t t, Meet mt,
+                          uint32_t frame_local) {
+    Shared& sh = *C.sh;
+    constexpr uint32_t kNW = kBT / 32;
+    const uint32_t d = mt.a + mt.b + 1;
+    if (d < 2) return true;
+    if (kDet && C.tid == 0) sh.ev_pos = atomicAdd(p.ev_cursor, static_cast<unsigned long long>(d - 1));
+    uint32_t cur = t, cmeta = 0;
+    const uint32_t tslot = S.find(t, cmeta);
+    unsigned long long csig = S.sigma(tslot);
+    __syncthreads();
+    const uint64_t ev_pos = kDet ? sh.ev_pos : 0;
+    uint32_t ds_cur = d;
+    for (uint32_t step = 0; ds_cur > 1; ++step) {
+        unsigned long long r = rng.next_below(csig);
+        bool want_t;
+        uint32_t want_dist;
+        if (m_is_t(cmeta)) {
+            const uint32_t k = m_dist(cmeta);
+            want_t = k < mt.b;
+            want_dist = k < mt.b ? k + 1 : mt.a;
+        } else {
+            want_t = false;
+            want_dist = m_dist(cmeta) - 1;
+        }
+        const uint32_t beg = C.off[cur], end = C.off[cur + 1];
+        bool found = false;
+        for (uint32_t base = beg; base < end; base += kBT) {
+            const uint32_t i = base + C.tid;
+            uint32_t q = 0, m = 0;
+            unsigned long long val = 0;
+            if (i < end) {
+                q = C.nbrs[i];
+                const uint32_t sl = S.find(q, m);
+                if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag)))
+                    val = S.sigma(sl);
+            }
+            C.back_edges += C.tid == 0 ? min(static_cast<uint32_t>(kBT), end - base) : 0;
+            unsigned long long lo = val;
+            uint32_t hi = 0;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const unsigned long long olo = __shfl_up_sync(kFull, lo, dd);
+                const uint32_t ohi = __shfl_up_sync(kFull, hi, dd);
+                if (C.lane >= static_cast<uint32_t>(dd)) add65(lo, hi, olo, ohi);
+            }
+            if (C.lane == 31) {
+                sh.wlo[C.warp] = lo;
+                sh.whi[C.warp] = hi;
+            }
+            if (C.tid == 0) sh.first = kNone;
+            __syncthreads();
+            unsigned long long tot_lo = 0;
+            uint32_t tot_hi = 0;
+            for (uint32_t w = 0; w < kNW; ++w) {
+                if (w == C.warp) add65(lo, hi, tot_lo, tot_hi);  // inclusive block prefix
+                add65(tot_lo, tot_hi, sh.wlo[w], sh.whi[w]);
+            }
+            const uint32_t ball = __ballot_sync(kFull, hi > 0 || r < lo);
+            if (ball && C.lane == static_cast<uint32_t>(__ffs(ball) - 1)) atomicMin(&sh.first, C.tid);
+            __syncthreads();
+            const uint32_t f = sh.first;
+            if (f != kNone) {
+                if (C.tid == f) {
+                    sh.ch = q;
+                    sh.chm = m;
+                    sh.chs = val;
+                }
+                __syncthreads();
+                cur = sh.ch;
+                cmeta = sh.chm;
+                csig = sh.chs;
+                found = true;
+                __syncthreads();
+                break;
+            }
+            r -= tot_lo;  // tot_hi == 0 here: otherwise some prefix would exceed r
+            __syncthreads();
+        }
+        if (!found) return false;
+        if (C.tid == 0) {
+            if (kDet) {
+                if (ev_pos + step < p.ev_cap)
+                    p.events[ev_pos + step] = (static_cast<unsigned long long>(cur) << 32) | frame_local;
+            } else {
+                atomicAdd(p.counts + cur, 1u);
+            }
+        }
+        ds_cur = m_is_t(cmeta) ? d - m_dist(cmeta) : m_dist(cmeta);
+    }
+    return true;
+}
+
+// Whole sample with one store. Returns 0 ok, 1 overflow (redo with the global
+// store), 2 inconsistent state.
+template <bool kDet, class Store>
+__device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t s, uint32_t t,
+                          uint32_t frame_local) {
+    Shared& sh = *C.sh;
+    S.begin(C.tid);
+    if (C.tid == 0) {
+        sh.inserted = 0;
+        sh.overflow = 0;
+    }
+    __syncthreads();
+    const Meet mt = bfs(C, S, s, t);
+    if (mt.status != 0) {
+        S.end(C, *C.sh);
+        return mt.status;
+    }
+    rebuild(C, S, mt.b);
+    const int rc = backtrack<kDet>(C, S, p, rng, t, mt, frame_local) ? 0 : 2;  // block-uniform
+    S.end(C, sh);
+    return rc;
+}
+
+template <bool kDet>
+__global__ void __launch_bounds__(kBT) sampler_cta_kernel(SamplerParams p) {
+    extern __shared__ unsigned long long dyn[];
+    __shared__ Shared sh;
+    Ctx C;
+    C.off = p.off;
+    C.nbrs = p.nbrs;
+    C.tid = threadIdx.x;
+    C.lane = threadIdx.x & 31;
+    C.warp = threadIdx.x >> 5;
+    C.sh = &sh;
+    C.edges = C.rebuild_edges = C.back_edges = C.verts = 0;
+    const uint32_t slot = blockIdx.x;
+
+    SmemStore sm;
+    const uint32_t H = p.hash_cap;
+    sm.km = dyn;
+    sm.sig = dyn + H;
+    sm.qcap = H / 2;
+    sm.qv = reinterpret_cast<uint32_t*>(dyn + 2 * H);
+    sm.qdeg = sm.qv + sm.qcap;
+    sm.tlev = sh.tlev_small;
+    sm.mask = H - 1;
+    sm.shift = 64 - (31 - __clz(H));
+    sm.limit = H / 2;
+    sm.level_cap = kSmemLevels;
+    sm.sh = &sh;
+
+    GlobalStore gs;
+    gs.st = p.state + 2ull * p.slot_stride * slot;
+    gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
+    gs.qdeg = reinterpret_cast<uint32_t*>(p.qrange + static_cast<size_t>(p.slot_stride) * slot);
+    gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
+    gs.tag = p.slot_tag[slot];
+    gs.qcap = p.n;
+    gs.level_cap = p.level_cap;
+
+    sm.clear_all(C.tid);
+    __syncthreads();
+    unsigned long long samples = 0, fallbacks = 0, errors = 0;
+    for (;;) {
+        if (C.tid == 0) sh.item = atomicAdd(p.ticket, 1ull);
+        __syncthreads();
+        const unsigned long long item = sh.item;
+        __syncthreads();
+        if (item >= p.num_items) break;
+        const uint64_t local = item * p.world + p.rank;
+        SplitMix64 rng(reseed(p.seed, p.first + local));
+        for (uint64_t i = 0; i < p.spf; ++i) {
+            ++samples;
+            const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
+            uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
+            if (t >= s) ++t;
+            if (__ldg(p.label + s) != __ldg(p.label + t)) continue;
+            int rc = 1;
+            if (p.use_smem) rc = run_sample<kDet>(C, sm, p, rng, s, t, static_cast<uint32_t>(local));
+            if (rc == 1) {
+                fallbacks += p.use_smem ? 1 : 0;
+                gs.tag += 1;
+                rc = run_sample<kDet>(C, gs, p, rng, s, t, static_cast<uint32_t>(local));
+            }
+            if (rc != 0) ++errors;
+        }
+    }
+    // per-thread counters: reduce across the block once
+    atomicAdd(p.stats + kStatEdges, C.edges + C.rebuild_edges + C.back_edges);
+    atomicAdd(p.stats + kStatRebuildEdges, C.rebuild_edges);
+    atomicAdd(p.stats + kStatBacktrackEdges, C.back_edges);
+    atomicAdd(p.stats + kStatVertices, C.verts);
+    if (C.tid == 0) {
+        p.slot_tag[slot] = gs.tag;
+        atomicAdd(p.stats + kStatSamples, samples);
+        atomicAdd(p.stats + kStatFallbacks, fallbacks);
+        if (errors) atomicAdd(p.stats + kStatErrors, errors);
+    }
+}
+

@@ -174,3 +174,22 @@ def test_sampler_variants_bit_exact(mode, monkeypatch, grid200):
     want = oracle.sample_frames(og2, 9, 1, 0, 40)
     for a, b in zip(got, want):
         np.testing.assert_array_equal(a, b)
+
+
+def test_cpp_dropin_tool_matches_oracle(tmp_path):
+    """tools/adsb_run.cpp (written only against include/adsamp_b200.hpp) reproduces
+    the reference CLI's score file (adsamp_cli.cpp:99-106 format) bit for bit."""
+    import subprocess
+    from pathlib import Path
+    tool = Path(__file__).resolve().parents[1] / "paper_1903_09422_b200" / "adsb_run"
+    path = tmp_path / "c1.edges"
+    datasets.write_edge_list(path, datasets.pairs("c1_er"))
+    out = tmp_path / "scores.csv"
+    res = subprocess.run([str(tool), "--graph", str(path), "--variant", "indexed", "--threads", "8", "--eps", "0.01",
+                          "--delta", "0.1", "--seed", "42", "--samples-per-frame", "1", "--output", str(out)],
+                         capture_output=True, text=True, check=True)
+    assert "tau: 10307  reason: eps_converged" in res.stdout
+    og = oracle.parse_file(path)
+    o = oracle.estimate_bc(og, 0.01, 0.1, spf=1, seed=42)
+    want = "vertex_id,score\n" + "".join("%d,%.10g\n" % (int(i), s) for i, s in zip(og.original_ids, o.scores))
+    assert out.read_text() == want
