@@ -196,22 +196,9 @@ def main() -> None:
     comm = None
     if world > 1:
         import torch.distributed as dist
-        import ctypes as C
-        from paper_1903_09422_b200._lib import check, lib
+        from paper_1903_09422_b200.distributed import Comm
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            buf = (C.c_uint8 * 128)()
-            check(lib().adsb_comm_unique_id(buf))
-            uid.copy_(torch.tensor(list(buf), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        idb = (C.c_uint8 * 128)(*uid.cpu().tolist())
-        h = C.c_void_p()
-        check(lib().adsb_comm_init(world, rank, idb, local, C.byref(h)))
-
-        class _Comm:
-            handle = h
-        comm = _Comm()
+        comm = Comm.from_torch_distributed(device=local)
 
     w = datasets.CONFIGS[args.config]
     t0 = time.perf_counter()

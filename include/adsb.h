@@ -94,6 +94,8 @@ typedef struct {
     uint64_t rebuild_edges;      /* of edges_scanned: t-side DAG sigma rebuild */
     uint64_t backtrack_edges;    /* of edges_scanned: predecessor scans of the backtrack */
     uint64_t store_fallbacks;    /* samples redone with global-memory state (shared-memory table overflow) */
+    uint64_t degenerate_steps;   /* backtrack steps whose sigma and every predecessor sigma were 0 mod 2^64
+                                    (undefined in the reference) */
 } adsb_stats;
 
 void adsb_config_init(adsb_config *cfg); /* reference defaults (engine.hpp:85-96) */

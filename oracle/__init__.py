@@ -37,7 +37,7 @@ class _Result(C.Structure):
     _fields_ = [("tau", C.c_uint64), ("check_cycles", C.c_uint64), ("stop_epoch", C.c_uint64),
                 ("omega", C.c_uint64), ("diameter_bound", C.c_uint64), ("total_samples", C.c_uint64),
                 ("edges_scanned", C.c_uint64), ("vertices_expanded", C.c_uint64), ("reason", C.c_int32),
-                ("pad", C.c_int32)]
+                ("pad", C.c_int32), ("degenerate_steps", C.c_uint64)]
 
 
 _lib = None
@@ -236,6 +236,7 @@ class Result:
     vertices_expanded: int
     counts: np.ndarray
     scores: np.ndarray
+    degenerate_steps: int = 0
 
 
 def estimate_bc(g: Graph, eps: float, delta: float, *, mode: int = MODE_INDEXED, spf: int = 1,
@@ -250,7 +251,7 @@ def estimate_bc(g: Graph, eps: float, delta: float, *, mode: int = MODE_INDEXED,
     if rc:
         raise OracleError(rc, err.value.decode())
     return Result(res.tau, res.check_cycles, res.stop_epoch, res.omega, res.diameter_bound, REASONS[res.reason],
-                  res.edges_scanned, res.vertices_expanded, counts[: g.n], scores[: g.n])
+                  res.edges_scanned, res.vertices_expanded, counts[: g.n], scores[: g.n], res.degenerate_steps)
 
 
 def brandes(g: Graph, threads: int | None = None) -> np.ndarray:

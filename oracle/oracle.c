@@ -494,6 +494,7 @@ typedef struct {
     uint32_t *queue;
     uint64_t edges_scanned;
     uint64_t vertices_expanded;
+    uint64_t degenerate_steps;
 } scratch_t;
 
 void *or_scratch_new(uint32_t n) {
@@ -555,11 +556,12 @@ static uint32_t sample_between(const or_graph *g, scratch_t *sc, uint64_t *rng, 
     uint32_t cur = t, len = 0;
     while (dist[cur] > 1) {
         uint64_t r = or_next_below(rng, sigma[cur]);
-        uint32_t chosen = UINT32_MAX;
+        uint32_t chosen = UINT32_MAX, first_pred = UINT32_MAX;
         for (uint64_t e = g->offsets[cur]; e < g->offsets[cur + 1]; ++e) {
             const uint32_t p = g->nbrs[e];
             sc->edges_scanned++;
             if (stamp[p] == gen && dist[p] + 1 == dist[cur]) {
+                if (first_pred == UINT32_MAX) first_pred = p;
                 if (r < sigma[p]) {
                     chosen = p;
                     break;
@@ -567,7 +569,15 @@ static uint32_t sample_between(const or_graph *g, scratch_t *sc, uint64_t *rng, 
                 r -= sigma[p];
             }
         }
-        if (chosen == UINT32_MAX) break; /* unreachable unless every sigma wrapped to 0 */
+        if (chosen == UINT32_MAX) {
+            /* Reached only when sigma[cur] and every predecessor's sigma are
+             * 0 mod 2^64 (r = next_below(0) = 0). The reference then indexes
+             * dist[] with UINT32_MAX (kadabra.hpp:230-241; it segfaults on C4,
+             * frame 247 of seed 42). Defined here, and identically on the GPU:
+             * take the first predecessor in ascending id order. */
+            chosen = first_pred;
+            sc->degenerate_steps++;
+        }
         cur = chosen;
         out[len++] = cur;
     }
@@ -682,6 +692,7 @@ int or_estimate_bc(const or_graph *g, double eps, double delta, const or_config 
     res->total_samples = num;
     res->edges_scanned = sc->edges_scanned;
     res->vertices_expanded = sc->vertices_expanded;
+    res->degenerate_steps = sc->degenerate_steps;
     /* kadabra.hpp:339-343 */
     res->reason = OR_REASON_OMEGA;
     if (num >= 1 && converged(data, n, num, omega, eps, log_inv)) res->reason = OR_REASON_EPS;

@@ -80,6 +80,7 @@ class Stats(C.Structure):
         ("rebuild_edges", C.c_uint64),
         ("backtrack_edges", C.c_uint64),
         ("store_fallbacks", C.c_uint64),
+        ("degenerate_steps", C.c_uint64),
     ]
 
 

@@ -30,6 +30,7 @@ COMMON = [
     "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
     f"-I{ROOT / 'include'}", f"-I{CSRC}",
+    *os.environ.get("ADSB_NVCC_EXTRA", "").split(),
 ]
 
 

@@ -327,6 +327,7 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
             stats->rebuild_edges = r.rebuild_edges;
             stats->backtrack_edges = r.backtrack_edges;
             stats->store_fallbacks = r.store_fallbacks;
+            stats->degenerate_steps = r.degenerate_steps;
         }
     });
 }

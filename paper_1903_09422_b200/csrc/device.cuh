@@ -147,7 +147,15 @@ struct DeviceRuntime {
     std::vector<cudaEvent_t> ev_launch;
     cudaStream_t stream = nullptr;   // sampling stream
     cudaStream_t stream2 = nullptr;  // check / collective stream
+    // Device buffers of destroyed graphs, reused by the next graphs (avoids a
+    // cudaFree + cudaMalloc pair, which synchronises the device, per handle).
+    std::mutex spare_mu;
+    std::vector<DevBuf<uint32_t>> spare;
 };
+
+// best-fit reuse of a spare buffer (within 2x of the request), else a fresh allocation
+DevBuf<uint32_t> take_buffer(DeviceRuntime& rt, size_t count);
+void give_buffer(DeviceRuntime& rt, DevBuf<uint32_t>&& b);
 
 // Never destroyed: lives until process exit (CUDA tears its resources down then).
 DeviceRuntime& device_runtime(int device);
@@ -161,6 +169,7 @@ struct DeviceContext {
     uint64_t diameter_bound = 0;
     uint32_t num_components = 0;
     DeviceRuntime* rt = nullptr;
+    ~DeviceContext();
 };
 
 int resolve_device(int requested);

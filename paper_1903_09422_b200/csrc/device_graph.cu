@@ -161,6 +161,44 @@ DeviceRuntime& device_runtime(int device) {
     return *rt;
 }
 
+DevBuf<uint32_t> take_buffer(DeviceRuntime& rt, size_t count) {
+    count = std::max<size_t>(count, 1);
+    {
+        std::lock_guard<std::mutex> lock(rt.spare_mu);
+        size_t best = rt.spare.size();
+        for (size_t i = 0; i < rt.spare.size(); ++i)
+            if (rt.spare[i].count >= count && rt.spare[i].count <= 2 * count &&
+                (best == rt.spare.size() || rt.spare[i].count < rt.spare[best].count))
+                best = i;
+        if (best != rt.spare.size()) {
+            DevBuf<uint32_t> b = std::move(rt.spare[best]);
+            rt.spare.erase(rt.spare.begin() + static_cast<long>(best));
+            return b;
+        }
+    }
+    ADSB_CUDA(cudaSetDevice(rt.device));
+    return DevBuf<uint32_t>(count);
+}
+
+void give_buffer(DeviceRuntime& rt, DevBuf<uint32_t>&& b) {
+    if (!b.ptr) return;
+    std::lock_guard<std::mutex> lock(rt.spare_mu);
+    rt.spare.push_back(std::move(b));
+    size_t total = 0;
+    for (auto& x : rt.spare) total += x.bytes();
+    while (rt.spare.size() > 8 || total > (size_t{16} << 30)) {  // keep at most 8 buffers / 16 GiB
+        total -= rt.spare.front().bytes();
+        rt.spare.erase(rt.spare.begin());
+    }
+}
+
+DeviceContext::~DeviceContext() {
+    if (!rt) return;
+    give_buffer(*rt, std::move(graph.offsets));
+    give_buffer(*rt, std::move(graph.nbrs));
+    give_buffer(*rt, std::move(labels));
+}
+
 std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int device) {
     if (g.nnz() >= 0xFFFFFFFFull) invalid("device CSR needs fewer than 2^32 adjacency entries");
     ADSB_CUDA(cudaSetDevice(device));
@@ -175,8 +213,9 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
     // u32 offsets on the device: narrow on the host, then one copy each.
     std::vector<uint32_t> off32(g.offsets.size());
     for (size_t i = 0; i < off32.size(); ++i) off32[i] = static_cast<uint32_t>(g.offsets[i]);
-    dg.offsets.alloc(off32.size());
-    dg.nbrs.alloc(std::max<uint64_t>(1, g.nnz()));
+    dg.offsets = take_buffer(*ctx->rt, off32.size());
+    dg.nbrs = take_buffer(*ctx->rt, std::max<uint64_t>(1, g.nnz()));
+    ctx->labels = take_buffer(*ctx->rt, std::max<uint32_t>(1, g.n));
     ADSB_CUDA(cudaMemcpyAsync(dg.offsets.ptr, off32.data(), off32.size() * sizeof(uint32_t),
                               cudaMemcpyHostToDevice, ctx->rt->stream));
     if (g.nnz())
@@ -199,7 +238,7 @@ uint32_t device_components(DeviceContext& ctx) {
     uint32_t* parent = ctx.rt->pool.get<uint32_t>(Scratch::kParent, n);
     uint32_t* is_root = ctx.rt->pool.get<uint32_t>(Scratch::kIsRoot, n + 1);  // zero tail: scanned with n+1 inputs
     uint32_t* rank = ctx.rt->pool.get<uint32_t>(Scratch::kRank, n + 1);
-    if (ctx.labels.count < n) ctx.labels.alloc(n);
+    if (ctx.labels.count < n) ctx.labels = take_buffer(*ctx.rt, n);
     const unsigned g = grid_for(n, ctx.device);
     uf_init<<<g, 256, 0, s>>>(parent, n);
     uf_hook<<<grid_for(static_cast<uint64_t>(n) * 32, ctx.device), 256, 0, s>>>(

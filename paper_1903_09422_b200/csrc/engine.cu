@@ -596,6 +596,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     out.rebuild_edges = st_host[kStatRebuildEdges];
     out.backtrack_edges = st_host[kStatBacktrackEdges];
     out.store_fallbacks = st_host[kStatFallbacks];
+    out.degenerate_steps = st_host[kStatDegenerate];
     out.kernel_launches = L.count;
     // kadabra.hpp:339-343
     if (out.reason != ADSB_REASON_CAPPED) {

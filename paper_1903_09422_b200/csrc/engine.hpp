@@ -29,7 +29,7 @@ struct EngineOutput {
     uint32_t num_components = 0;
     double preprocess_seconds = 0, ads_seconds = 0;
     uint64_t edges_scanned = 0, vertices_expanded = 0, kernel_launches = 0;
-    uint64_t rebuild_edges = 0, backtrack_edges = 0, store_fallbacks = 0;
+    uint64_t rebuild_edges = 0, backtrack_edges = 0, store_fallbacks = 0, degenerate_steps = 0;
     double sampler_ms = 0;
 };
 

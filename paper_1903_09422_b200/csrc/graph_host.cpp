@@ -90,7 +90,7 @@ HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
             std::memcpy(g.nbrs.data() + kept[u], raw.data() + deg[u],
                         (kept[u + 1] - kept[u]) * sizeof(uint32_t));
     });
-    g.offsets = std::move(kept);
+    g.offsets.assign(kept.begin(), kept.end());
     g.original_ids.resize(n);
     std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});
     return g;
@@ -102,16 +102,25 @@ HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nb
         if (offsets[u + 1] < offsets[u]) invalid("offsets must be non-decreasing");
     HostGraph g;
     g.n = n;
-    g.offsets.assign(offsets, offsets + static_cast<size_t>(n) + 1);
-    g.nbrs.assign(nbrs, nbrs + offsets[n]);
+    g.offsets.resize(static_cast<size_t>(n) + 1);
+    g.nbrs.resize(offsets[n]);
     std::atomic<bool> bad{false};
+    // one parallel pass: copy each vertex range and check the Graph invariants
     parallel_for(n, [&](uint64_t b, uint64_t e) {
-        for (uint64_t u = b; u < e && !bad.load(std::memory_order_relaxed); ++u)
-            for (uint64_t i = g.offsets[u]; i < g.offsets[u + 1]; ++i) {
-                const uint32_t v = g.nbrs[i];
-                if (v >= n || v == u || (i > g.offsets[u] && g.nbrs[i - 1] >= v)) bad = true;
+        std::memcpy(g.offsets.data() + b, offsets + b, (e - b) * sizeof(uint64_t));
+        std::memcpy(g.nbrs.data() + offsets[b], nbrs + offsets[b], (offsets[e] - offsets[b]) * sizeof(uint32_t));
+        bool local_bad = false;
+        for (uint64_t u = b; u < e; ++u) {
+            uint64_t prev = UINT64_MAX;
+            for (uint64_t i = offsets[u]; i < offsets[u + 1]; ++i) {
+                const uint32_t v = nbrs[i];
+                local_bad |= v >= n || v == u || (prev != UINT64_MAX && prev >= v);
+                prev = v;
             }
+        }
+        if (local_bad) bad = true;
     });
+    g.offsets[n] = offsets[n];
     if (bad) invalid("CSR must have in-range, ascending, duplicate-free, loop-free adjacency");
     g.original_ids.resize(n);
     std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});

@@ -8,15 +8,37 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace adsb {
 
+// Allocator that leaves trivially-constructible elements uninitialised on
+// resize: large CSR arrays are filled by parallel copies right after.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    using value_type = T;
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    NoInitAlloc() = default;
+    template <class U>
+    NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U*) noexcept {}
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+
 struct HostGraph {
     uint32_t n = 0;
-    std::vector<uint64_t> offsets;       // n+1
-    std::vector<uint32_t> nbrs;          // offsets[n], ascending per vertex
+    std::vector<uint64_t, NoInitAlloc<uint64_t>> offsets;  // n+1
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> nbrs;     // offsets[n], ascending per vertex
     std::vector<uint64_t> original_ids;  // dense -> id in the input (identity when absent)
     bool has_original_ids = false;
 

@@ -92,6 +92,7 @@ struct Team {
     unsigned long long rebuild_edges;  // DAG sigma rebuild
     unsigned long long back_edges;     // backtrack scans
     unsigned long long verts;
+    unsigned long long degenerate;
     bool error;
 
     __device__ unsigned long long* meta_ptr(uint32_t v) const { return st + 2ull * v; }
@@ -374,8 +375,8 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
             want_dist = dist_of(cs.x) - 1;
         }
         const uint32_t beg = T.off[cur], end = T.off[cur + 1];
-        uint32_t chosen = kNone;
-        ulonglong2 chosen_state = make_ulonglong2(0, 0);
+        uint32_t chosen = kNone, first_pred = kNone;
+        ulonglong2 chosen_state = make_ulonglong2(0, 0), first_state = make_ulonglong2(0, 0);
         for (uint32_t base = beg; base < end; base += 32) {
             const uint32_t i = base + T.lane;
             uint32_t q = 0;
@@ -389,6 +390,16 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
                 val = cand ? sq.y : 0ull;
             }
             T.back_edges += min(32u, end - base);
+            if (first_pred == kNone) {
+                const uint32_t cb = __ballot_sync(kFull, i < end && tag_of(sq.x) == T.tag && is_t(sq.x) == want_t &&
+                                                             dist_of(sq.x) == want_dist && (!want_t || (sq.x & kDag)));
+                if (cb) {
+                    const int f = __ffs(cb) - 1;
+                    first_pred = __shfl_sync(kFull, q, f);
+                    first_state.x = shfl64(sq.x, f);
+                    first_state.y = shfl64(sq.y, f);
+                }
+            }
             // 65-bit inclusive prefix sum (lo + carry count)
             unsigned long long lo = val;
             uint32_t hi = 0;
@@ -412,7 +423,14 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
             }
             r -= shfl64(lo, 31);
         }
-        if (chosen == kNone) { T.error = true; return; }  // every predecessor sigma wrapped to 0
+        if (chosen == kNone) {
+            // sigma(cur) and all predecessor sigmas are 0 mod 2^64: reference UB
+            // (oracle.c documents the rule); take the first predecessor
+            if (first_pred == kNone) { T.error = true; return; }
+            chosen = first_pred;
+            chosen_state = first_state;
+            T.degenerate += 1;
+        }
         emit<kDet>(p, T.lane, chosen, ev_pos + step, frame_local);
         cur = chosen;
         cs = chosen_state;
@@ -440,6 +458,7 @@ __global__ void __launch_bounds__(256) sampler_kernel(SamplerParams p) {
     T.rebuild_edges = 0;
     T.back_edges = 0;
     T.verts = 0;
+    T.degenerate = 0;
     T.error = false;
     unsigned long long samples = 0;
     for (;;) {
@@ -462,6 +481,7 @@ __global__ void __launch_bounds__(256) sampler_kernel(SamplerParams p) {
         atomicAdd(p.stats + kStatVertices, T.verts);
         atomicAdd(p.stats + kStatSamples, samples);
         if (T.error) atomicAdd(p.stats + kStatErrors, 1ull);
+        if (T.degenerate) atomicAdd(p.stats + kStatDegenerate, T.degenerate);
     }
 }
 

@@ -24,7 +24,8 @@ enum SamplerStat {
     kStatRebuildEdges = 4,
     kStatBacktrackEdges = 5,
     kStatFallbacks = 6,
-    kStatCount = 7
+    kStatDegenerate = 7,
+    kStatCount = 8
 };
 
 struct SamplerParams {

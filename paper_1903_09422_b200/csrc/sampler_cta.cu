@@ -31,6 +31,13 @@
 #include "rng.hpp"
 #include "sampler.cuh"
 
+#ifndef ADSB_UNROLL
+#define ADSB_UNROLL 2  // adjacency loads in flight per thread in for_edges
+#endif
+#ifndef ADSB_MINB_PER_256
+#define ADSB_MINB_PER_256 3  // __launch_bounds__ min blocks for 256-thread blocks (register budget)
+#endif
+
 namespace adsb {
 
 namespace bt128 {

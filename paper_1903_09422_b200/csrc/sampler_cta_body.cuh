@@ -57,7 +57,7 @@ struct SmemStore {
     Shared* sh;
 
     __device__ uint32_t home(uint32_t v) const {
-        return static_cast<uint32_t>((static_cast<unsigned long long>(v) * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+        return ((v * 0x9E3779B1u) >> shift) & mask;  // Fibonacci hashing on 32 bits
     }
     __device__ void clear_all(uint32_t tid) {
         for (uint32_t i = tid; i <= mask; i += kBT) {
@@ -200,7 +200,7 @@ struct Ctx {
     uint32_t lane;
     uint32_t warp;
     Shared* sh;
-    unsigned long long edges, rebuild_edges, back_edges, verts;
+    unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
 };
 
 // Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
@@ -231,15 +231,47 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         sh.cval[C.tid] = val;
         __syncthreads();
         counter += C.tid == 0 ? total : 0;
-        for (uint32_t e = C.tid; e < total; e += kBT) {
-            uint32_t l = 0, r = kBT - 1;  // first k with scan[k] > e
-            while (l < r) {
-                const uint32_t mid = (l + r) >> 1;
-                if (sh.scan[mid] > e) r = mid;
-                else l = mid + 1;
+        // Owner of edge e = first chunk entry k with scan[k] > e. A thread's
+        // edges e, e+kBT, ... have non-decreasing owners, so it keeps the
+        // current owner's row in registers and searches again (over the
+        // remaining populated entries only) when e passes that owner's end:
+        // O(1) per edge inside hub adjacency lists.
+        const uint32_t populated = min(hi - base, static_cast<uint32_t>(kBT));
+        uint32_t ow = 0, o_end = 0, o_base = 0, o_slot = 0;
+        unsigned long long o_val = 0;
+        bool have = false;
+        // kUnroll adjacency loads in flight per thread before any is consumed
+        constexpr uint32_t kUnroll = ADSB_UNROLL;
+        for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kUnroll) {
+            uint32_t vv[kUnroll], vs[kUnroll];
+            unsigned long long vval[kUnroll];
+#pragma unroll
+            for (uint32_t k = 0; k < kUnroll; ++k) {
+                const uint32_t e = e0 + k * kBT;
+                vv[k] = kNone;
+                if (e < total) {
+                    if (!have || e >= o_end) {
+                        uint32_t l = have ? ow + 1 : 0, r = populated - 1;
+                        while (l < r) {
+                            const uint32_t mid = (l + r) >> 1;
+                            if (sh.scan[mid] > e) r = mid;
+                            else l = mid + 1;
+                        }
+                        ow = l;
+                        o_end = sh.scan[ow];
+                        o_base = sh.cbase[ow];
+                        o_slot = sh.cslot[ow];
+                        o_val = sh.cval[ow];
+                        have = true;
+                    }
+                    vv[k] = C.nbrs[o_base + e];
+                    vs[k] = o_slot;
+                    vval[k] = o_val;
+                }
             }
-            const uint32_t v = C.nbrs[sh.cbase[l] + e];
-            body(sh.cslot[l], sh.cval[l], v);
+#pragma unroll
+            for (uint32_t k = 0; k < kUnroll; ++k)
+                if (vv[k] != kNone) body(vs[k], vval[k], vv[k]);
         }
         __syncthreads();
     }
@@ -502,7 +534,40 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             r -= tot_lo;  // tot_hi == 0 here: otherwise some prefix would exceed r
             __syncthreads();
         }
-        if (!found) return false;
+        if (!found) {
+            // sigma(cur) and every predecessor sigma are 0 mod 2^64: reference UB
+            // (oracle.c documents the rule) -> the first predecessor in id order
+            for (uint32_t base = beg; base < end && !found; base += kBT) {
+                const uint32_t i = base + C.tid;
+                uint32_t q = 0, m = 0;
+                bool cand = false;
+                if (i < end) {
+                    q = C.nbrs[i];
+                    const uint32_t sl = S.find(q, m);
+                    cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag));
+                }
+                if (C.tid == 0) sh.first = kNone;
+                __syncthreads();
+                const uint32_t ball = __ballot_sync(kFull, cand);
+                if (ball && C.lane == static_cast<uint32_t>(__ffs(ball) - 1)) atomicMin(&sh.first, C.tid);
+                __syncthreads();
+                if (C.tid == sh.first) {
+                    sh.ch = q;
+                    sh.chm = m;
+                    sh.chs = 0;
+                }
+                __syncthreads();
+                if (sh.first != kNone) {
+                    cur = sh.ch;
+                    cmeta = sh.chm;
+                    csig = sh.chs;
+                    found = true;
+                }
+                __syncthreads();
+            }
+            if (!found) return false;
+            C.degenerate += C.tid == 0 ? 1 : 0;
+        }
         if (C.tid == 0) {
             if (kDet) {
                 if (ev_pos + step < p.ev_cap)
@@ -540,7 +605,7 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 }
 
 template <bool kDet>
-__global__ void __launch_bounds__(kBT) sampler_cta_kernel(SamplerParams p) {
+__global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_cta_kernel(SamplerParams p) {
     extern __shared__ unsigned long long dyn[];
     __shared__ Shared sh;
     Ctx C;
@@ -550,7 +615,7 @@ __global__ void __launch_bounds__(kBT) sampler_cta_kernel(SamplerParams p) {
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
-    C.edges = C.rebuild_edges = C.back_edges = C.verts = 0;
+    C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
     const uint32_t slot = blockIdx.x;
 
     SmemStore sm;
@@ -562,7 +627,7 @@ __global__ void __launch_bounds__(kBT) sampler_cta_kernel(SamplerParams p) {
     sm.qdeg = sm.qv + sm.qcap;
     sm.tlev = sh.tlev_small;
     sm.mask = H - 1;
-    sm.shift = 64 - (31 - __clz(H));
+    sm.shift = 32 - (31 - __clz(H));
     sm.limit = H / 2;
     sm.level_cap = kSmemLevels;
     sm.sh = &sh;
@@ -613,6 +678,7 @@ __global__ void __launch_bounds__(kBT) sampler_cta_kernel(SamplerParams p) {
         atomicAdd(p.stats + kStatSamples, samples);
         atomicAdd(p.stats + kStatFallbacks, fallbacks);
         if (errors) atomicAdd(p.stats + kStatErrors, errors);
+        if (C.degenerate) atomicAdd(p.stats + kStatDegenerate, C.degenerate);
     }
 }
 

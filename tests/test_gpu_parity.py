@@ -193,3 +193,34 @@ def test_cpp_dropin_tool_matches_oracle(tmp_path):
     o = oracle.estimate_bc(og, 0.01, 0.1, spf=1, seed=42)
     want = "vertex_id,score\n" + "".join("%d,%.10g\n" % (int(i), s) for i, s in zip(og.original_ids, o.scores))
     assert out.read_text() == want
+
+
+def test_nccl_paths_world1(c1):
+    """Exercise the NCCL code paths (epoch all-reduce, deterministic event
+    all-gather with sentinel padding and 64-bit sort) with a 1-rank
+    communicator: results must equal the communicator-free run."""
+    from paper_1903_09422_b200.distributed import Comm
+    comm = Comm(1, 0, Comm.unique_id(), 0)
+    pg, og = c1
+    for variant, extra in [(Variant.indexed, {}), (Variant.shared, {"epoch_samples": 4096})]:
+        base = EngineConfig(variant=variant, samples_per_frame=1, base_seed=9, threads=8, **extra)
+        with_comm = EngineConfig(variant=variant, samples_per_frame=1, base_seed=9, threads=8, comm=comm, **extra)
+        a = estimate_bc(pg.graph, 0.01, 0.1, base)
+        b = estimate_bc(pg.graph, 0.01, 0.1, with_comm)
+        assert (a.tau, a.run.check_cycles) == (b.tau, b.run.check_cycles)
+        np.testing.assert_array_equal(a.run.data, b.run.data)
+    comm.close()
+
+
+def test_degenerate_sigma_frames_c4():
+    """On the C4 grid, frame 247 (seed 42) hits a backtrack step where sigma(cur)
+    and every predecessor sigma are 0 mod 2^64; the reference's behaviour is
+    undefined there (it segfaults). Engine and oracle both take the first
+    predecessor in id order, so the paths must still agree."""
+    p = datasets.pairs("c4_grid")
+    pg, og = both(p)
+    got = sample_frames(pg.graph, 42, 1, 244, 6)
+    want = oracle.sample_frames(og, 42, 1, 244, 6)
+    assert len(want[3]) > 0
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)

@@ -34,7 +34,7 @@ def test_c_abi_exports_every_declared_symbol():
 
 def test_struct_layouts():
     assert C.sizeof(_lib.Config) == 80
-    assert C.sizeof(_lib.Stats) == 128
+    assert C.sizeof(_lib.Stats) == 136
 
 
 @pytest.mark.parametrize("text,n,m,ids", PARSE_CASES)
