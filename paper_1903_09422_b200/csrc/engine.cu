@@ -33,6 +33,7 @@
 
 #include "comm.hpp"
 #include "engine.hpp"
+#include "rule.cuh"
 #include "sampler.cuh"
 
 namespace adsb {
@@ -72,31 +73,8 @@ namespace {
 constexpr uint32_t kNoStop = 0xFFFFFFFFu;
 // word offsets into DeviceContext::pinned (words 0..15 belong to the BFS level counts)
 constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
-              kPinAdapt = 72;
+              kPinAdapt = 72, kPinCtl = 80;  // kPinCtl: 9 words
 static_assert(kStatCount <= 8, "pinned staging layout");
-
-struct RuleParams {
-    uint64_t omega;
-    double omega_d;
-    double log_inv;
-    double eps;
-};
-
-// kadabra.hpp:59-67 + 148-151 at the maximum count, IEEE _rn ops only.
-__device__ bool rule_passes(uint64_t max_count, uint64_t tau, const RuleParams& r) {
-    if (tau >= r.omega) return true;
-    const double tau_d = __ull2double_rn(tau);
-    const double b = __ddiv_rn(__ull2double_rn(max_count), tau_d);
-    const double two_b_w_l = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, b), r.omega_d), r.log_inv);
-    const double scale = __ddiv_rn(r.log_inv, tau_d);
-    const double w_t = __ddiv_rn(r.omega_d, tau_d);
-    const double tf = __dsub_rn(1.0 / 3.0, w_t);
-    const double f = __dmul_rn(scale, __dadd_rn(tf, __dsqrt_rn(__dadd_rn(__dmul_rn(tf, tf), two_b_w_l))));
-    if (f > r.eps) return false;
-    const double tg = __dadd_rn(1.0 / 3.0, w_t);
-    const double g = __dmul_rn(scale, __dadd_rn(tg, __dsqrt_rn(__dadd_rn(__dmul_rn(tg, tg), two_b_w_l))));
-    return !(g > r.eps);
-}
 
 // K4a: value of each sorted event = count of v after its frame; per-frame max
 __global__ void k_event_values(const unsigned long long* __restrict__ sorted, uint64_t count,
@@ -474,6 +452,58 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         out.check_cycles = done;
         out.tau = done * spf;
         out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
+    } else if (!opt.comm && arena(ctx).kind == 1 && !std::getenv("ADSB_NO_FUSED")) {
+        // ---- cumulative epochs, fused: one persistent launch folds finished
+        // epochs in order and evaluates the rule on the device (no host round
+        // trip per epoch), so epochs can be as small as the reference's check
+        // interval and the run stops within ~K epochs + one sample per block.
+        const uint64_t B = opt.epoch_samples ? opt.epoch_samples : 1024;
+        uint64_t max_epochs = (out.omega + B - 1) / B;
+        if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
+        max_epochs = std::max<uint64_t>(max_epochs, 1);
+        const uint32_t K = 8;
+        unsigned long long* ctl = ctx.rt->pool.get<unsigned long long>(Scratch::kCtl, kCtlWords);
+        uint32_t* ring_cnt = ctx.rt->pool.get<uint32_t>(Scratch::kRingCnt, static_cast<size_t>(K) * n);
+        uint32_t* ring_list = ctx.rt->pool.get<uint32_t>(Scratch::kRingList, static_cast<size_t>(K) * n);
+        uint32_t* ring_len = ctx.rt->pool.get<uint32_t>(Scratch::kRingLen, K);
+        ADSB_CUDA(cudaMemsetAsync(ctl, 0, kCtlWords * sizeof(unsigned long long), s1));
+        ADSB_CUDA(cudaMemsetAsync(ctl + kCtlStop, 0xFF, sizeof(unsigned long long), s1));
+        ADSB_CUDA(cudaMemsetAsync(ring_cnt, 0, static_cast<size_t>(K) * n * sizeof(uint32_t), s1));
+        ADSB_CUDA(cudaMemsetAsync(ring_len, 0, K * sizeof(uint32_t), s1));
+        SamplerParams p = base_params(ctx, opt.seed, 1);
+        p.stats = stats;
+        p.ctl = ctl;
+        p.ring_cnt = ring_cnt;
+        p.ring_list = ring_list;
+        p.ring_len = ring_len;
+        p.total = total;
+        p.epoch_b = B;
+        p.max_epochs = max_epochs;
+        p.ring_k = K;
+        p.rule = rule;
+        ADSB_CUDA(cudaEventRecord(e0, s1));
+        launch_sampler_fused(p, s1);
+        ADSB_CUDA(cudaEventRecord(e1, s1));
+        L.count++;
+        unsigned long long* ctl_h = ctx.rt->pinned.ptr + kPinCtl;
+        ADSB_CUDA(cudaMemcpyAsync(ctl_h, ctl, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
+        ADSB_CUDA(cudaStreamSynchronize(s1));
+        float ms = 0;
+        ADSB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        out.sampler_ms = ms;
+        const uint64_t stop = ctl_h[kCtlStop];
+        if (stop == ~0ull) fail(ADSB_ERR_LOGIC, "fused epoch pipeline exited without a stop decision");
+        if (ctl_h[kCtlCapped]) out.reason = ADSB_REASON_CAPPED;
+        out.tau = (stop + 1) * B;
+        out.check_cycles = stop + 1;
+        out.stop_epoch = stop + 1;
+        ADSB_CUDA(cudaMemcpyAsync(ctl_h + 8, stats + kStatSamples, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
+        ADSB_CUDA(cudaStreamSynchronize(s1));
+        out.total_samples = ctl_h[8];
+        if (trace_enabled())
+            std::fprintf(stderr, "[adsb] fused epochs: B %llu stop epoch %llu drawn %llu t=%.3f ms\n",
+                         static_cast<unsigned long long>(B), static_cast<unsigned long long>(stop),
+                         static_cast<unsigned long long>(out.total_samples), 1e3 * ads.seconds());
     } else {
         // ---- cumulative epoch pipeline
         uint64_t B = opt.epoch_samples;

@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "rule.cuh"
+
 namespace adsb {
 
 // Per-vertex state word layout (one u64 "meta" + one u64 sigma per vertex and slot):
@@ -26,6 +28,18 @@ enum SamplerStat {
     kStatFallbacks = 6,
     kStatDegenerate = 7,
     kStatCount = 8
+};
+
+// Control words of the fused epoch pipeline (SamplerParams::ctl).
+enum FusedCtl {
+    kCtlTicket = 0,   // next sample index
+    kCtlFolded = 1,   // epochs folded into `total` so far
+    kCtlStop = 2,     // epoch at which the run stopped (~0 while running)
+    kCtlLock = 3,     // fold lock
+    kCtlMax = 4,      // running max of `total`
+    kCtlCapped = 5,   // 1 when stopped by max_cycles rather than by the rule
+    kCtlDone = 8,     // kCtlDone + k: samples finished in ring slot k
+    kCtlWords = 8 + 64
 };
 
 struct SamplerParams {
@@ -61,6 +75,17 @@ struct SamplerParams {
     // epoch output: per-vertex counts of this epoch
     uint32_t* counts;
     unsigned long long* stats;  // kStatCount
+    // fused epoch mode (one GPU): the kernel folds finished epochs in order and
+    // evaluates the stopping rule itself
+    unsigned long long* ctl;    // kCtlWords
+    uint32_t* ring_cnt;         // ring_k * n per-epoch counts
+    uint32_t* ring_list;        // ring_k * n distinct vertices touched per epoch
+    uint32_t* ring_len;         // ring_k
+    uint32_t* total;            // n running counts
+    uint64_t epoch_b;
+    uint64_t max_epochs;
+    uint32_t ring_k;
+    RuleParams rule;
 };
 
 // Warp-team sampler (sampler.cu): slots = resident warps.
@@ -70,6 +95,8 @@ void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_
 size_t sampler_cta_smem_bytes(uint32_t hash_cap);
 int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads);
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+// single-launch epoch pipeline with device-side folding and stopping (block teams)
+void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream);
 
 enum class SamplerKind { kWarp, kBlock };
 SamplerKind sampler_kind();  // ADSB_SAMPLER=warp|block (default block)

@@ -32,13 +32,31 @@
 #include "sampler.cuh"
 
 #ifndef ADSB_UNROLL
-#define ADSB_UNROLL 2  // adjacency loads in flight per thread in for_edges
+#define ADSB_UNROLL 1  // adjacency loads in flight per thread in for_edges
 #endif
 #ifndef ADSB_MINB_PER_256
-#define ADSB_MINB_PER_256 3  // __launch_bounds__ min blocks for 256-thread blocks (register budget)
+#define ADSB_MINB_PER_256 4  // __launch_bounds__ min blocks for 256-thread blocks (register budget)
+#endif
+
+#ifdef ADSB_DEBUG_CHECKS
+#include <cstdio>
+#define ADSB_DCHECK(cond, ...)                                                              \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("ADSB_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+                   blockIdx.x, threadIdx.x, #cond);                                         \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define ADSB_DCHECK(cond, ...) \
+    do {                       \
+    } while (0)
 #endif
 
 namespace adsb {
+
+constexpr int kModeDet = 0, kModeEpoch = 1, kModeFused = 2;
 
 namespace bt128 {
 constexpr int kBT = 128;
@@ -62,10 +80,12 @@ void allow_big_smem(K kernel) {
 void configure_once() {
     static bool done = false;
     if (done) return;
-    allow_big_smem(bt128::sampler_cta_kernel<true>);
-    allow_big_smem(bt128::sampler_cta_kernel<false>);
-    allow_big_smem(bt256::sampler_cta_kernel<true>);
-    allow_big_smem(bt256::sampler_cta_kernel<false>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeDet>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeEpoch>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeFused>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeDet>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeFused>);
     done = true;
 }
 }  // namespace
@@ -75,9 +95,9 @@ int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads) {
     const size_t dyn = sampler_cta_smem_bytes(hash_cap);
     int blocks = 0;
     if (block_threads == 128)
-        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<true>, 128, dyn));
+        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<kModeDet>, 128, dyn));
     else
-        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<true>, 256, dyn));
+        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet>, 256, dyn));
     return blocks;
 }
 
@@ -85,12 +105,20 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
     configure_once();
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
     if (p.block_threads == 128) {
-        if (deterministic) bt128::sampler_cta_kernel<true><<<p.slots, 128, dyn, stream>>>(p);
-        else bt128::sampler_cta_kernel<false><<<p.slots, 128, dyn, stream>>>(p);
+        if (deterministic) bt128::sampler_cta_kernel<kModeDet><<<p.slots, 128, dyn, stream>>>(p);
+        else bt128::sampler_cta_kernel<kModeEpoch><<<p.slots, 128, dyn, stream>>>(p);
     } else {
-        if (deterministic) bt256::sampler_cta_kernel<true><<<p.slots, 256, dyn, stream>>>(p);
-        else bt256::sampler_cta_kernel<false><<<p.slots, 256, dyn, stream>>>(p);
+        if (deterministic) bt256::sampler_cta_kernel<kModeDet><<<p.slots, 256, dyn, stream>>>(p);
+        else bt256::sampler_cta_kernel<kModeEpoch><<<p.slots, 256, dyn, stream>>>(p);
     }
+    ADSB_CUDA(cudaGetLastError());
+}
+
+void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
+    configure_once();
+    const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
+    if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused><<<p.slots, 128, dyn, stream>>>(p);
+    else bt256::sampler_cta_kernel<kModeFused><<<p.slots, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
 }
 

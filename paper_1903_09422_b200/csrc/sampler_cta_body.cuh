@@ -34,6 +34,8 @@ struct Shared {
     uint32_t ch, chm;                 // backtrack: chosen predecessor and its meta
     unsigned long long chs;           // backtrack: chosen predecessor's sigma
     unsigned long long ev_pos;
+    unsigned long long fold_epoch;    // fused mode: epoch being folded
+    uint32_t fold_len, fold_max, flag;
 };
 
 // ---------------------------------------------------------------------------
@@ -141,6 +143,7 @@ struct SmemStore {
         }
     }
     static constexpr bool kSigmaPreZeroed = true;  // claim and sigma accumulation share one pass
+    static constexpr bool kSpeculativeClaims = false;  // meeting-level claims would overflow the table
     __device__ void zero_sigma(uint32_t) {}
     __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(&sig[slot], x); }
     __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], static_cast<unsigned long long>(kMetaDag)); }
@@ -185,6 +188,7 @@ struct GlobalStore {
         return v;
     }
     static constexpr bool kSigmaPreZeroed = false;  // stale sigma: zero on claim, accumulate after a barrier
+    static constexpr bool kSpeculativeClaims = true;  // no capacity limit: probe and claim in one pass
     __device__ void zero_sigma(uint32_t slot) { st[2ull * slot + 1] = 0ull; }
     __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(st + 2ull * slot + 1, x); }
     __device__ void set_dag(uint32_t slot) { atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)); }
@@ -201,6 +205,7 @@ struct Ctx {
     uint32_t warp;
     Shared* sh;
     unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
+    uint32_t n;
 };
 
 // Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
@@ -217,6 +222,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         if (i < hi) {
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
+            ADSB_DCHECK(u < C.n);
             o = C.off[u];
             deg = C.off[u + 1] - o;
             uint32_t meta;
@@ -265,6 +271,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                         have = true;
                     }
                     vv[k] = C.nbrs[o_base + e];
+                    ADSB_DCHECK(vv[k] < C.n);
                     vs[k] = o_slot;
                     vval[k] = o_val;
                 }
@@ -311,7 +318,90 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     uint32_t s_lo = 0, s_hi = 1, t_lo = 0, t_hi = 1, a = 0, b = 0;
     unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
     for (;;) {
-        if (deg_s <= deg_t) {
+        if (deg_s <= deg_t && Store::kSpeculativeClaims) {
+            // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
+            // Claims made on the meeting level are harmless (never predecessors).
+            C.verts += C.tid == 0 ? s_hi - s_lo : 0;
+            bool met = false;
+            __syncthreads();  // every thread has read the previous level's degsum
+            if (C.tid == 0) sh.degsum = 0;
+            __syncthreads();
+            unsigned long long my_deg = 0;
+            for_edges(C, S, s_lo, s_hi, false, C.edges,
+                      [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
+                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                          bool ins;
+                          uint32_t m;
+                          const uint32_t sl = S.claim(v, a + 1, ins, m);
+                          if (ins) {
+                              S.zero_sigma(sl);
+                              const uint32_t pos = atomicAdd(&sh.s_cnt, 1u);
+                              const uint32_t dg = C.off[v + 1] - C.off[v];
+                              ADSB_DCHECK(pos + sh.t_cnt < S.qcap);
+                              S.qv[pos] = v;
+                              S.qdeg[pos] = dg;
+                              my_deg += dg;
+                          } else if (m_is_t(m) && m_dist(m) == b) {
+                              S.add_sigma(sl, su);
+                              if (!(m & kMetaDag)) S.set_dag(sl);
+                              met = true;
+                          }
+                      });
+            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            if (__syncthreads_or(met)) return {a, b, 0};
+            for_edges(C, S, s_lo, s_hi, false, C.edges,
+                      [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
+                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                          uint32_t m;
+                          const uint32_t sl = S.find(v, m);
+                          if (sl != kNone && !m_is_t(m) && m_dist(m) == a + 1) S.add_sigma(sl, su);
+                      });
+            s_lo = s_hi;
+            s_hi = sh.s_cnt;
+            deg_s = sh.degsum;
+            a += 1;
+            if (s_lo == s_hi) return {a, b, 2};
+        } else if (deg_s > deg_t && Store::kSpeculativeClaims) {
+            // ---- t-side level b, one pass: claim level b+1 and detect the meeting
+            C.verts += C.tid == 0 ? t_hi - t_lo : 0;
+            bool met = false;
+            __syncthreads();  // every thread has read the previous level's degsum
+            if (C.tid == 0) sh.degsum = 0;
+            __syncthreads();
+            unsigned long long my_deg = 0;
+            const uint32_t meta_new = kMetaT | (b + 1);
+            for_edges(C, S, t_lo, t_hi, true, C.edges,
+                      [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
+                      [&](uint32_t su_slot, unsigned long long, uint32_t v) {
+                          bool ins;
+                          uint32_t m;
+                          const uint32_t sl = S.claim(v, meta_new, ins, m);
+                          if (ins) {
+                              S.zero_sigma(sl);
+                              const uint32_t j = atomicAdd(&sh.t_cnt, 1u);
+                              const uint32_t dg = C.off[v + 1] - C.off[v];
+                              ADSB_DCHECK(j + sh.s_cnt < S.qcap);
+                              S.qv[S.tpos(j)] = v;
+                              S.qdeg[S.tpos(j)] = dg;
+                              my_deg += dg;
+                          } else if (!m_is_t(m) && m_dist(m) == a) {
+                              S.add_sigma(su_slot, S.sigma(sl));
+                              S.set_dag(su_slot);
+                              met = true;
+                          }
+                      });
+            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            if (__syncthreads_or(met)) return {a, b, 0};
+            t_lo = t_hi;
+            t_hi = sh.t_cnt;
+            deg_t = sh.degsum;
+            b += 1;
+            if (b + 2 > S.level_cap) return {a, b, 1};
+            ADSB_DCHECK(b + 1 < S.level_cap);
+            if (C.tid == 0) S.tlev[b + 1] = t_hi;
+            __syncthreads();
+            if (t_lo == t_hi) return {a, b, 2};
+        } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
             C.verts += C.tid == 0 ? s_hi - s_lo : 0;
             bool met = false;
@@ -416,6 +506,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             deg_t = sh.degsum;
             b += 1;
             if (b + 2 > S.level_cap) return {a, b, 1};
+            ADSB_DCHECK(b + 1 < S.level_cap);
             if (C.tid == 0) S.tlev[b + 1] = t_hi;
             __syncthreads();
             if (t_lo == t_hi) return {a, b, 2};
@@ -454,13 +545,14 @@ __device__ __forceinline__ void add65(unsigned long long& lo, uint32_t& hi, unsi
 // `r -= sigma[p]` scan. All threads draw the same r from their copy of the
 // stream. Returns false on an inconsistent state (every predecessor sigma
 // wrapped to 0), which the reference leaves undefined.
-template <bool kDet, class Store>
+template <int kMode, class Store>
 __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t t, Meet mt,
                           uint32_t frame_local) {
     Shared& sh = *C.sh;
     constexpr uint32_t kNW = kBT / 32;
     const uint32_t d = mt.a + mt.b + 1;
     if (d < 2) return true;
+    constexpr bool kDet = kMode == kModeDet;
     if (kDet && C.tid == 0) sh.ev_pos = atomicAdd(p.ev_cursor, static_cast<unsigned long long>(d - 1));
     uint32_t cur = t, cmeta = 0;
     const uint32_t tslot = S.find(t, cmeta);
@@ -569,11 +661,16 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             C.degenerate += C.tid == 0 ? 1 : 0;
         }
         if (C.tid == 0) {
-            if (kDet) {
+            if (kMode == kModeDet) {
                 if (ev_pos + step < p.ev_cap)
                     p.events[ev_pos + step] = (static_cast<unsigned long long>(cur) << 32) | frame_local;
-            } else {
+            } else if (kMode == kModeEpoch) {
                 atomicAdd(p.counts + cur, 1u);
+            } else {
+                // fused: frame_local is the ring slot; record first touches for the fold
+                const size_t base = static_cast<size_t>(frame_local) * p.n;
+                if (atomicAdd(p.ring_cnt + base + cur, 1u) == 0u)
+                    p.ring_list[base + atomicAdd(p.ring_len + frame_local, 1u)] = cur;
             }
         }
         ds_cur = m_is_t(cmeta) ? d - m_dist(cmeta) : m_dist(cmeta);
@@ -583,7 +680,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 
 // Whole sample with one store. Returns 0 ok, 1 overflow (redo with the global
 // store), 2 inconsistent state.
-template <bool kDet, class Store>
+template <int kMode, class Store>
 __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t s, uint32_t t,
                           uint32_t frame_local) {
     Shared& sh = *C.sh;
@@ -599,12 +696,115 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         return mt.status;
     }
     rebuild(C, S, mt.b);
-    const int rc = backtrack<kDet>(C, S, p, rng, t, mt, frame_local) ? 0 : 2;  // block-uniform
+    const int rc = backtrack<kMode>(C, S, p, rng, t, mt, frame_local) ? 0 : 2;  // block-uniform
     S.end(C, sh);
     return rc;
 }
 
-template <bool kDet>
+// One sample (s, t draw + traversal + backtrack) with the shared-memory store
+// first and the global store as fallback. Returns 0 ok or an error code.
+template <int kMode>
+__device__ void one_sample(Ctx& C, SmemStore& sm, GlobalStore& gs, const SamplerParams& p, SplitMix64& rng,
+                           uint32_t frame_local, unsigned long long& fallbacks, unsigned long long& errors) {
+    const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
+    uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
+    if (t >= s) ++t;
+    if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
+    int rc = 1;
+    if (p.use_smem) rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+    if (rc == 1) {
+        fallbacks += p.use_smem ? 1 : 0;
+        gs.tag += 1;
+        rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
+    }
+    if (rc != 0) ++errors;
+}
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* a) {
+    return *reinterpret_cast<const volatile unsigned long long*>(a);
+}
+
+// Fused epoch pipeline: fold finished epochs strictly in order (the reference's
+// cumulative check, engine.hpp:267-341, at epoch granularity) and evaluate the
+// stopping rule on the device. At most one block folds at a time (lock); a
+// block that finishes an epoch while another folds leaves it to that block,
+// which re-checks for completed successors after releasing the lock.
+__device__ void fold_chain(Ctx& C, const SamplerParams& p) {
+    Shared& sh = *C.sh;
+    unsigned long long* ctl = p.ctl;
+    const unsigned long long kNoEpoch = ~0ull;
+    for (;;) {
+        if (C.tid == 0) sh.flag = atomicCAS(ctl + kCtlLock, 0ull, 1ull) == 0ull ? 1u : 0u;
+        __syncthreads();
+        const bool got = sh.flag != 0;
+        __syncthreads();
+        if (!got) return;
+        for (;;) {
+            if (C.tid == 0) {
+                __threadfence();
+                const unsigned long long f = vload(ctl + kCtlFolded);
+                const uint32_t k = static_cast<uint32_t>(f % p.ring_k);
+                const bool go = vload(ctl + kCtlStop) == kNoEpoch && f < p.max_epochs &&
+                                vload(ctl + kCtlDone + k) == p.epoch_b;
+                sh.fold_epoch = go ? f : kNoEpoch;
+                sh.fold_len = go ? *reinterpret_cast<volatile uint32_t*>(p.ring_len + k) : 0u;
+                sh.fold_max = 0;
+                __threadfence();
+            }
+            __syncthreads();
+            const unsigned long long f = sh.fold_epoch;
+            const uint32_t len = sh.fold_len;
+            if (f == kNoEpoch) {
+                __syncthreads();
+                break;
+            }
+            const uint32_t k = static_cast<uint32_t>(f % p.ring_k);
+            uint32_t* cnt = p.ring_cnt + static_cast<size_t>(k) * p.n;
+            const uint32_t* list = p.ring_list + static_cast<size_t>(k) * p.n;
+            uint32_t local = 0;
+            for (uint32_t j = C.tid; j < len; j += kBT) {
+                const uint32_t v = __ldcg(list + j);
+                const uint32_t c = atomicExch(cnt + v, 0u);
+                const uint32_t tot = __ldcg(p.total + v) + c;
+                __stcg(p.total + v, tot);
+                local = max(local, tot);
+            }
+            if (local) atomicMax(&sh.fold_max, local);
+            __syncthreads();
+            if (C.tid == 0) {
+                const unsigned long long m = max(vload(ctl + kCtlMax), static_cast<unsigned long long>(sh.fold_max));
+                ctl[kCtlMax] = m;
+                const bool pass = rule_passes(m, (f + 1) * p.epoch_b, p.rule);
+                p.ring_len[k] = 0;
+                ctl[kCtlDone + k] = 0;
+                if (pass) {
+                    ctl[kCtlStop] = f;
+                } else if (f + 1 >= p.max_epochs) {
+                    ctl[kCtlCapped] = 1;
+                    ctl[kCtlStop] = f;
+                }
+                __threadfence();
+                atomicExch(ctl + kCtlFolded, f + 1);  // publishes the reset ring slot
+                __threadfence();
+            }
+            __syncthreads();
+        }
+        if (C.tid == 0) {
+            __threadfence();
+            atomicExch(ctl + kCtlLock, 0ull);
+            __threadfence();
+            const unsigned long long f = vload(ctl + kCtlFolded);
+            sh.flag = vload(ctl + kCtlStop) == kNoEpoch && f < p.max_epochs &&
+                      vload(ctl + kCtlDone + f % p.ring_k) == p.epoch_b ? 1u : 0u;
+        }
+        __syncthreads();
+        const bool again = sh.flag != 0;
+        __syncthreads();
+        if (!again) return;
+    }
+}
+
+template <int kMode>
 __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_cta_kernel(SamplerParams p) {
     extern __shared__ unsigned long long dyn[];
     __shared__ Shared sh;
@@ -616,6 +816,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
     C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
+    C.n = p.n;
     const uint32_t slot = blockIdx.x;
 
     SmemStore sm;
@@ -644,28 +845,55 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
     sm.clear_all(C.tid);
     __syncthreads();
     unsigned long long samples = 0, fallbacks = 0, errors = 0;
-    for (;;) {
-        if (C.tid == 0) sh.item = atomicAdd(p.ticket, 1ull);
-        __syncthreads();
-        const unsigned long long item = sh.item;
-        __syncthreads();
-        if (item >= p.num_items) break;
-        const uint64_t local = item * p.world + p.rank;
-        SplitMix64 rng(reseed(p.seed, p.first + local));
-        for (uint64_t i = 0; i < p.spf; ++i) {
-            ++samples;
-            const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
-            uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
-            if (t >= s) ++t;
-            if (__ldg(p.label + s) != __ldg(p.label + t)) continue;
-            int rc = 1;
-            if (p.use_smem) rc = run_sample<kDet>(C, sm, p, rng, s, t, static_cast<uint32_t>(local));
-            if (rc == 1) {
-                fallbacks += p.use_smem ? 1 : 0;
-                gs.tag += 1;
-                rc = run_sample<kDet>(C, gs, p, rng, s, t, static_cast<uint32_t>(local));
+    if (kMode != kModeFused) {
+        for (;;) {
+            if (C.tid == 0) sh.item = atomicAdd(p.ticket, 1ull);
+            __syncthreads();
+            const unsigned long long item = sh.item;
+            __syncthreads();
+            if (item >= p.num_items) break;
+            const uint64_t local = item * p.world + p.rank;
+            SplitMix64 rng(reseed(p.seed, p.first + local));
+            for (uint64_t i = 0; i < p.spf; ++i) {
+                ++samples;
+                one_sample<kMode>(C, sm, gs, p, rng, static_cast<uint32_t>(local), fallbacks, errors);
             }
-            if (rc != 0) ++errors;
+        }
+    } else {
+        // Sample i belongs to epoch i / B and ring slot (i / B) % K. A block may
+        // start epoch e only once epoch e - K has been folded (its slot is free);
+        // every earlier epoch's samples are already held by running blocks, so
+        // the wait always ends (one persistent grid, all blocks resident).
+        for (;;) {
+            if (C.tid == 0) {
+                unsigned long long i = atomicAdd(p.ctl + kCtlTicket, 1ull);
+                const unsigned long long e = i / p.epoch_b;
+                for (;;) {
+                    if (e > vload(p.ctl + kCtlStop) || e >= p.max_epochs) {
+                        i = ~0ull;
+                        break;
+                    }
+                    if (e < vload(p.ctl + kCtlFolded) + p.ring_k) break;
+                    __nanosleep(200);
+                }
+                sh.item = i;
+            }
+            __syncthreads();
+            const unsigned long long item = sh.item;
+            __syncthreads();
+            if (item == ~0ull) break;
+            const uint32_t k = static_cast<uint32_t>((item / p.epoch_b) % p.ring_k);
+            SplitMix64 rng(reseed(p.seed, item));
+            ++samples;
+            one_sample<kMode>(C, sm, gs, p, rng, k, fallbacks, errors);
+            if (C.tid == 0) {
+                __threadfence();  // this sample's counts before its completion
+                sh.flag = atomicAdd(p.ctl + kCtlDone + k, 1ull) + 1 == p.epoch_b ? 1u : 0u;
+            }
+            __syncthreads();
+            const bool completed = sh.flag != 0;
+            __syncthreads();
+            if (completed) fold_chain(C, p);
         }
     }
     // per-thread counters: reduce across the block once
@@ -681,4 +909,3 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
         if (C.degenerate) atomicAdd(p.stats + kStatDegenerate, C.degenerate);
     }
 }
-

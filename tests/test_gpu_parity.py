@@ -224,3 +224,28 @@ def test_degenerate_sigma_frames_c4():
     assert len(want[3]) > 0
     for a, b in zip(got, want):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("B", [64, 1024])
+def test_epoch_block_teams_fused_and_host_driven(fused, B, monkeypatch):
+    """Block-team epoch pipeline, fused (device-side in-order folds + stopping
+    rule in one persistent launch) and host-driven (double-buffered epochs on
+    two streams): both must equal the oracle's cumulative-epoch restatement."""
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    if not fused:
+        monkeypatch.setenv("ADSB_NO_FUSED", "1")
+    else:
+        monkeypatch.delenv("ADSB_NO_FUSED", raising=False)
+    for name, eps in [("er100", 0.05), ("c1", 0.01)]:
+        pairs = datasets.pairs("c1_er") if name == "c1" else SMALL_GRAPHS[name]()
+        pg, og = both(pairs)
+        cfg = EngineConfig(variant=Variant.shared, threads=4, base_seed=13, epoch_samples=B)
+        r = estimate_bc(pg.graph, eps, 0.1, cfg)
+        o = oracle.estimate_bc(og, eps, 0.1, mode=oracle.MODE_EPOCH, epoch_samples=B, seed=13)
+        assert (r.tau, r.run.check_cycles, r.reason.name) == (o.tau, o.check_cycles, o.reason), name
+        np.testing.assert_array_equal(r.run.data, o.counts)
+        assert r.run.total_samples >= r.tau
+    cap = EngineConfig(variant=Variant.shared, threads=4, base_seed=13, epoch_samples=B, max_cycles=3)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cap)
+    assert r.tau == 3 * B and r.reason.name == "capped"
