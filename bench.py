@@ -115,7 +115,7 @@ def run_reference(args, world: int, rank: int) -> None:
         except Exception:
             pass
     path = datasets.edge_list_file(w.name, ROOT / "build" / "graphs")
-    per_rep_samples = args.ref_samples_per_core * cores
+    per_rep_samples = CPU_SAMPLES_PER_CORE.get(w.name, args.ref_samples_per_core) * cores
     variant = "indexed" if w.variant == "indexed" else "barrier"
     if oracle.ref_available():
         kind = "reference"
@@ -146,10 +146,16 @@ def run_reference(args, world: int, rank: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+# Reference samples per host core for one capped CPU run (~2-10 s each): the
+# reference's forward BFS costs 0.38 / 39 / 234 / 174 / 5340 ms per sample on
+# C1..C5.
+CPU_SAMPLES_PER_CORE = {"c1_er": 2000, "c2_rmat18": 100, "c3_ba": 20, "c4_grid": 30, "c5_rmat24": 1}
+
+
 def cpu_baseline(w, path) -> dict:
     import oracle
     cores = os.cpu_count() or 1
-    per = 100 * cores
+    per = CPU_SAMPLES_PER_CORE.get(w.name, 20) * cores
     try:
         if not oracle.ref_available():
             oracle.build()
@@ -176,6 +182,7 @@ def main() -> None:
     ap.add_argument("--impl", default="adsb", choices=["adsb", "reference"])
     ap.add_argument("--epoch-samples", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-samples-per-core", type=int, default=25)
     args = ap.parse_args()
@@ -320,8 +327,13 @@ def main() -> None:
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
-        path = datasets.edge_list_file(w.name, ROOT / "build" / "graphs")
-        line["cpu_baseline"] = cpu_baseline(w, path)
+        if g.num_edges() > 50_000_000 and not args.force_cpu_baseline:
+            line["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": "skipped: the reference parses the multi-GB edge list single-threaded "
+                                              "(minutes); pass --force-cpu-baseline"}
+        else:
+            path = datasets.edge_list_file(w.name, ROOT / "build" / "graphs")
+            line["cpu_baseline"] = cpu_baseline(w, path)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

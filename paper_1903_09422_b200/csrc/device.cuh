@@ -88,7 +88,7 @@ struct PinnedBuf {
 enum class Scratch : int {
     kParent, kIsRoot, kRank, kCubTemp, kFlags, kDist, kFrontA, kFrontB, kLevelCounts, kBest,
     kTotal, kStats, kScal, kBaseMax, kStopIdx, kEvents, kSorted, kGathered, kFrameMax, kRunMax,
-    kSortTemp, kEpochCnt, kDmax, kFlagDev, kTickets, kNcclScalar, kCtl, kRingCnt, kRingList, kRingLen, kCount
+    kSortTemp, kEpochCnt, kDmax, kFlagDev, kTickets, kNcclScalar, kCtl, kRingCnt, kRingList, kRingLen, kEvents2, kScal2, kCount
 };
 
 struct ScratchPool {
@@ -118,7 +118,6 @@ struct DeviceGraph {
 struct SamplerArena {
     int kind = 1;            // SamplerKind (0 warp teams, 1 block teams)
     uint32_t hash_cap = 0;   // block teams: shared-memory hash capacity
-    bool use_smem = true;    // block teams: disabled when most samples overflow the table
     uint32_t block_threads = 256;
     uint32_t slots = 0;
     uint32_t n = 0;
@@ -166,6 +165,7 @@ struct DeviceContext {
     DevBuf<uint32_t> labels;  // component labels (reference numbering)
     bool labels_ready = false;
     bool dub_ready = false;   // the graph is immutable: labels and D_ub are computed once per handle
+    int use_smem = -1;        // block teams: -1 undecided, 0 global-store-only, 1 shared-memory table first
     uint64_t diameter_bound = 0;
     uint32_t num_components = 0;
     DeviceRuntime* rt = nullptr;

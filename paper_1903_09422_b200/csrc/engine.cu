@@ -73,7 +73,7 @@ namespace {
 constexpr uint32_t kNoStop = 0xFFFFFFFFu;
 // word offsets into DeviceContext::pinned (words 0..15 belong to the BFS level counts)
 constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
-              kPinAdapt = 72, kPinCtl = 80;  // kPinCtl: 9 words
+              kPinAdapt = 72, kPinCtl = 80, kPinCursor = 96;  // kPinCtl: 9 words; kPinCursor: 2 words
 static_assert(kStatCount <= 8, "pinned staging layout");
 
 // K4a: value of each sorted event = count of v after its frame; per-frame max
@@ -179,14 +179,12 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     uint32_t block_threads = 256;
     if (const char* e = std::getenv("ADSB_BLOCK")) block_threads = std::strtoul(e, nullptr, 10) == 128 ? 128 : 256;
     if (hash_cap < 64 || (hash_cap & (hash_cap - 1))) invalid("ADSB_HASH_CAP must be a power of two >= 64");
-    const bool use_smem = !std::getenv("ADSB_NO_SMEM");
     const int k = kind == SamplerKind::kWarp ? 0 : 1;
     DeviceRuntime& rt = *ctx.rt;
     rt.active = k;
     std::unique_ptr<SamplerArena>& slot = rt.arena[k];
     if (slot && slot->n >= n && slot->level_cap >= level_cap && slot->hash_cap == hash_cap &&
         slot->block_threads == block_threads) {
-        if (!use_smem) slot->use_smem = false;
         return;
     }
     const uint32_t cap_n = slot ? std::max(slot->n, n) : n;
@@ -210,7 +208,6 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->kind = k;
     a->hash_cap = hash_cap;
     a->block_threads = block_threads;
-    a->use_smem = use_smem;
     a->slots = static_cast<uint32_t>(slots);
     a->n = cap_n;
     a->level_cap = cap_levels;
@@ -245,7 +242,8 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.tlev = a.tlev.ptr;
     p.slot_tag = a.slot_tag.ptr;
     p.hash_cap = a.hash_cap;
-    p.use_smem = a.use_smem ? 1u : 0u;
+    p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
+    p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
     p.block_threads = a.block_threads;
     return p;
 }
@@ -258,11 +256,11 @@ struct Launches {
 // overflow it (their balls are too large); results do not depend on the store.
 void adapt_store(DeviceContext& ctx, const unsigned long long* stats, cudaStream_t s) {
     SamplerArena& a = arena(ctx);
-    if (a.kind == 0 || !a.use_smem) return;
+    if (a.kind == 0 || ctx.use_smem != 1) return;
     unsigned long long* h = ctx.rt->pinned.ptr + kPinAdapt;
     ADSB_CUDA(cudaMemcpyAsync(h, stats, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     ADSB_CUDA(cudaStreamSynchronize(s));
-    if (h[kStatSamples] >= 256 && h[kStatFallbacks] * 2 > h[kStatSamples]) a.use_smem = false;
+    if (h[kStatSamples] >= 256 && h[kStatFallbacks] * 2 > h[kStatSamples]) ctx.use_smem = 0;
 }
 
 // One deterministic batch through the sampler; grows the event buffer until it fits.
@@ -325,6 +323,11 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     const double log_inv = std::log(1.0 / delta_v);                 // kadabra.hpp:123
     const uint32_t level_cap = static_cast<uint32_t>(std::min<uint64_t>(out.diameter_bound + 3, n + 2));
     ensure_arena(ctx, level_cap);
+    if (ctx.use_smem < 0) {
+        // Deep graphs (grid: D_ub 8182) need far more t-levels than the table
+        // tracks and far larger balls than it holds: go global-only at once.
+        ctx.use_smem = std::getenv("ADSB_NO_SMEM") || out.diameter_bound > 128 ? 0 : 1;
+    }
     out.preprocess_seconds = pre.seconds();
     if (trace_enabled())
         std::fprintf(stderr, "[adsb] preprocess: components %.3f ms, D_ub %.3f ms, arena %.3f ms (kind %d, slots %u)\n",
@@ -348,7 +351,169 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     // work units that keep every team busy: warps are many and light, blocks few and heavy
     const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).slots;
 
-    if (opt.deterministic) {
+    if (opt.deterministic && !opt.comm && !std::getenv("ADSB_NO_DET_PIPELINE")) {
+        // ---- deterministic frames, pipelined: while the host reads batch b's
+        // event count and stream 2 runs its ordered cutoff, stream 1 already
+        // samples batch b+1 (speculatively; wasted if b stops). Two event
+        // buffers alternate; a buffer is reused only after its cutoff applied.
+        const uint64_t spf = opt.spf;
+        uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
+        if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
+        frame_limit = std::max<uint64_t>(frame_limit, 1);
+        uint32_t* base_max = ctx.rt->pool.get<uint32_t>(Scratch::kBaseMax, 1);
+        uint32_t* stop_idx = ctx.rt->pool.get<uint32_t>(Scratch::kStopIdx, 1);
+        uint32_t* stop_h = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinStop);
+        unsigned long long* cursor_h = ctx.rt->pinned.ptr + kPinCursor;
+        ADSB_CUDA(cudaMemsetAsync(base_max, 0, sizeof(uint32_t), s1));
+        const Scratch ev_id[2] = {Scratch::kEvents, Scratch::kEvents2};
+        unsigned long long* ev_buf[2] = {ctx.rt->pool.get<unsigned long long>(ev_id[0], 1 << 20),
+                                         ctx.rt->pool.get<unsigned long long>(ev_id[1], 1 << 20)};
+        unsigned long long* scal2 = ctx.rt->pool.get<unsigned long long>(Scratch::kScal2, 4);
+        if (!ctx.rt->ev_samp[0]) {
+            for (int i = 0; i < 2; ++i) {
+                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_samp[i], cudaEventDisableTiming));
+                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_chk[i], cudaEventDisableTiming));
+            }
+            ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_stat, cudaEventDisableTiming));
+        }
+        cudaEvent_t* ev_sampled = ctx.rt->ev_samp;
+        cudaEvent_t* ev_free = ctx.rt->ev_chk;
+        bool slot_used[2] = {false, false};
+        struct Batch {
+            uint64_t first = 0, F = 0;
+            int slot = 0;
+            uint64_t launch = 0;
+        };
+        uint64_t next_first = 0, sampled_frames = 0, launches = 0;
+        auto plan = [&](Batch& b, int slot) -> bool {
+            if (next_first >= frame_limit) return false;
+            uint64_t F = std::max<uint64_t>(2 * team_slots, next_first);
+            F = std::min<uint64_t>(F, frame_limit - next_first);
+            F = std::min<uint64_t>(F, 1ull << 30);
+            b.first = next_first;
+            b.F = F;
+            b.slot = slot;
+            next_first += F;
+            return true;
+        };
+        auto enqueue = [&](Batch& b) {
+            const int j = b.slot;
+            if (slot_used[j]) ADSB_CUDA(cudaStreamWaitEvent(s1, ev_free[j], 0));
+            slot_used[j] = true;
+            ADSB_CUDA(cudaMemsetAsync(scal2 + 2 * j, 0, 2 * sizeof(unsigned long long), s1));
+            SamplerParams p = base_params(ctx, opt.seed, spf);
+            p.first = b.first;
+            p.num_items = b.F;
+            p.ticket = scal2 + 2 * j;
+            p.ev_cursor = scal2 + 2 * j + 1;
+            p.events = ev_buf[j];
+            p.ev_cap = ctx.rt->pool.capacity<unsigned long long>(ev_id[j]);
+            p.stats = stats;
+            while (ctx.rt->ev_launch.size() < 2 * (launches + 1)) {
+                cudaEvent_t ev;
+                ADSB_CUDA(cudaEventCreate(&ev));
+                ctx.rt->ev_launch.push_back(ev);
+            }
+            b.launch = launches++;
+            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * b.launch], s1));
+            launch_sampler(static_cast<SamplerKind>(arena(ctx).kind == 0 ? 0 : 1), true, p, s1);
+            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * b.launch + 1], s1));
+            ADSB_CUDA(cudaMemcpyAsync(cursor_h + j, scal2 + 2 * j + 1, sizeof(unsigned long long),
+                                      cudaMemcpyDeviceToHost, s1));
+            ADSB_CUDA(cudaEventRecord(ev_sampled[j], s1));
+            sampled_frames += b.F;
+            L.count++;
+        };
+        int vbits = 1;
+        while (vbits < 32 && (1ull << vbits) < n) ++vbits;
+        const int end_bit = 32 + vbits;
+        Batch cur, nxt;
+        plan(cur, 0);
+        enqueue(cur);
+        bool have_next = plan(nxt, 1);
+        if (have_next) enqueue(nxt);
+        uint64_t done = 0;
+        bool stopped = false;
+        for (;;) {
+            const int j = cur.slot;
+            ADSB_CUDA(cudaEventSynchronize(ev_sampled[j]));
+            uint64_t E = cursor_h[j];
+            if (E > ctx.rt->pool.capacity<unsigned long long>(ev_id[j])) {
+                // event buffer overflow: redo this batch alone into a larger buffer
+                ADSB_CUDA(cudaStreamSynchronize(s1));
+                ADSB_CUDA(cudaStreamSynchronize(s2));
+                ev_buf[j] = ctx.rt->pool.get<unsigned long long>(ev_id[j], E + E / 4 + 1024);
+                slot_used[j] = false;
+                sampled_frames -= cur.F;
+                enqueue(cur);
+                ADSB_CUDA(cudaEventSynchronize(ev_sampled[j]));
+                E = cursor_h[j];
+            }
+            const uint64_t F = cur.F;
+            unsigned long long* ev = ev_buf[j];
+            unsigned long long* sorted = ctx.rt->pool.get<unsigned long long>(Scratch::kSorted, E);
+            uint32_t* frame_max = ctx.rt->pool.get<uint32_t>(Scratch::kFrameMax, F);
+            uint32_t* run_max = ctx.rt->pool.get<uint32_t>(Scratch::kRunMax, F);
+            size_t tb = 0, tb2 = 0;
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, ev, sorted, E, 0, end_bit, s2));
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, frame_max, run_max, MaxOp(),
+                                                     static_cast<int64_t>(F), s2));
+            tb = std::max(tb, tb2);
+            uint8_t* temp = ctx.rt->pool.get<uint8_t>(Scratch::kSortTemp, tb);
+            ADSB_CUDA(cudaStreamWaitEvent(s2, ev_sampled[j], 0));
+            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(temp, tb, ev, sorted, E, 0, end_bit, s2));
+            ADSB_CUDA(cudaMemsetAsync(frame_max, 0, F * sizeof(uint32_t), s2));
+            k_event_values<<<grid_for(E, ctx.device), 256, 0, s2>>>(sorted, E, total, frame_max);
+            ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp, tb, frame_max, run_max, MaxOp(), static_cast<int64_t>(F), s2));
+            ADSB_CUDA(cudaMemsetAsync(stop_idx, 0xFF, sizeof(uint32_t), s2));
+            k_find_stop<<<grid_for(F, ctx.device), 256, 0, s2>>>(run_max, static_cast<uint32_t>(F), base_max, done,
+                                                                 spf, rule, stop_idx);
+            ADSB_CUDA(cudaMemcpyAsync(stop_h, stop_idx, sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
+            ADSB_CUDA(cudaStreamSynchronize(s2));
+            L.count += 3;
+            const uint32_t stop_host = *stop_h;
+            uint32_t limit = static_cast<uint32_t>(F - 1);
+            if (stop_host != kNoStop) {
+                limit = stop_host;
+                stopped = true;
+            } else if (done + F >= frame_limit) {
+                stopped = true;  // max_cycles cap
+                out.reason = ADSB_REASON_CAPPED;
+            }
+            k_apply<<<grid_for(E, ctx.device), 256, 0, s2>>>(ev, E, limit, total);
+            k_update_base<<<1, 32, 0, s2>>>(run_max, limit, base_max);
+            ADSB_CUDA(cudaEventRecord(ev_free[j], s2));
+            L.count += 2;
+            if (trace_enabled())
+                std::fprintf(stderr, "[adsb] det batch (pipelined): frames %llu..%llu events %llu stop %d t=%.3f ms\n",
+                             static_cast<unsigned long long>(done), static_cast<unsigned long long>(done + F),
+                             static_cast<unsigned long long>(E), stop_host == kNoStop ? -1 : static_cast<int>(stop_host),
+                             1e3 * ads.seconds());
+            if (stopped) {
+                done += static_cast<uint64_t>(limit) + 1;
+                break;
+            }
+            done += F;
+            if (!have_next) {  // cannot happen: the last batch reaches frame_limit and stops above
+                out.reason = ADSB_REASON_CAPPED;
+                break;
+            }
+            cur = nxt;
+            have_next = plan(nxt, 1 - cur.slot);
+            if (have_next) enqueue(nxt);
+        }
+        ADSB_CUDA(cudaStreamSynchronize(s1));  // a speculative batch may still be running
+        ADSB_CUDA(cudaStreamSynchronize(s2));
+        for (uint64_t i = 0; i < launches; ++i) {
+            float ms = 0;
+            ADSB_CUDA(cudaEventElapsedTime(&ms, ctx.rt->ev_launch[2 * i], ctx.rt->ev_launch[2 * i + 1]));
+            out.sampler_ms += ms;
+        }
+        out.total_samples = sampled_frames * spf;
+        out.check_cycles = done;
+        out.tau = done * spf;
+        out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
+    } else if (opt.deterministic) {
         const uint64_t spf = opt.spf;
         uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
         if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
@@ -581,10 +746,9 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             const bool pass = flag_host[k] != 0;
             if (e == 0) {
                 ADSB_CUDA(cudaEventSynchronize(ctx.rt->ev_stat));
-                SamplerArena& ar = arena(ctx);
-                if (ar.kind == 1 && ar.use_smem && stat0[kStatSamples] >= 256 &&
+                if (arena(ctx).kind == 1 && ctx.use_smem == 1 && stat0[kStatSamples] >= 256 &&
                     stat0[kStatFallbacks] * 2 > stat0[kStatSamples])
-                    ar.use_smem = false;
+                    ctx.use_smem = 0;
             }
             if (trace_enabled())
                 std::fprintf(stderr, "[adsb] epoch %llu checked: pass %d t=%.3f ms\n", static_cast<unsigned long long>(e),
@@ -652,6 +816,7 @@ void sample_frames(DeviceContext& ctx, uint64_t seed, uint64_t spf, uint64_t fir
     device_components(ctx);
     const uint64_t dub = device_diameter_bound(ctx);
     ensure_arena(ctx, static_cast<uint32_t>(std::min<uint64_t>(dub + 3, ctx.graph.n + 2)));
+    if (ctx.use_smem < 0) ctx.use_smem = std::getenv("ADSB_NO_SMEM") || dub > 128 ? 0 : 1;
     unsigned long long* events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, 1 << 16);
     unsigned long long* scal = ctx.rt->pool.get<unsigned long long>(Scratch::kScal, 4);
     unsigned long long* stats = ctx.rt->pool.get<unsigned long long>(Scratch::kStats, kStatCount);

@@ -56,6 +56,7 @@ struct SamplerParams {
     uint32_t hash_cap;     // block sampler: shared-memory hash capacity (power of two)
     uint32_t use_smem;     // block sampler: try the shared-memory store first
     uint32_t block_threads; // block sampler: 128 or 256
+    uint32_t global_grid;   // block sampler: resident blocks of the global-store-only variant
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode
@@ -95,6 +96,7 @@ void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_
 size_t sampler_cta_smem_bytes(uint32_t hash_cap);
 int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads);
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
+int sampler_global_blocks_per_sm();
 // single-launch epoch pipeline with device-side folding and stopping (block teams)
 void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream);
 

@@ -27,6 +27,8 @@
 // block prefix sum over the ascending-neighbour candidates per round.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
+
 #include "device.cuh"
 #include "rng.hpp"
 #include "sampler.cuh"
@@ -80,12 +82,15 @@ void allow_big_smem(K kernel) {
 void configure_once() {
     static bool done = false;
     if (done) return;
-    allow_big_smem(bt128::sampler_cta_kernel<kModeDet>);
-    allow_big_smem(bt128::sampler_cta_kernel<kModeEpoch>);
-    allow_big_smem(bt128::sampler_cta_kernel<kModeFused>);
-    allow_big_smem(bt256::sampler_cta_kernel<kModeDet>);
-    allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch>);
-    allow_big_smem(bt256::sampler_cta_kernel<kModeFused>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeDet, false>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeEpoch, false>);
+    allow_big_smem(bt128::sampler_cta_kernel<kModeFused, false>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeDet, false>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, false>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeFused, false>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeDet, true>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, true>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeFused, true>);
     done = true;
 }
 }  // namespace
@@ -95,21 +100,37 @@ int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads) {
     const size_t dyn = sampler_cta_smem_bytes(hash_cap);
     int blocks = 0;
     if (block_threads == 128)
-        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<kModeDet>, 128, dyn));
+        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<kModeDet, false>, 128, dyn));
     else
-        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet>, 256, dyn));
+        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet, false>, 256, dyn));
+    return blocks;
+}
+
+// Global-store-only variant (no shared-memory table): used when the table is
+// switched off for a graph. 128 registers, 2 blocks/SM, 4 loads in flight.
+int sampler_global_blocks_per_sm() {
+    configure_once();
+    int blocks = 0;
+    ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet, true>, 256, 0));
     return blocks;
 }
 
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream) {
     configure_once();
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
+    if (!p.use_smem) {
+        const unsigned grid = std::min<unsigned>(p.slots, p.global_grid);
+        if (deterministic) bt256::sampler_cta_kernel<kModeDet, true><<<grid, 256, 0, stream>>>(p);
+        else bt256::sampler_cta_kernel<kModeEpoch, true><<<grid, 256, 0, stream>>>(p);
+        ADSB_CUDA(cudaGetLastError());
+        return;
+    }
     if (p.block_threads == 128) {
-        if (deterministic) bt128::sampler_cta_kernel<kModeDet><<<p.slots, 128, dyn, stream>>>(p);
-        else bt128::sampler_cta_kernel<kModeEpoch><<<p.slots, 128, dyn, stream>>>(p);
+        if (deterministic) bt128::sampler_cta_kernel<kModeDet, false><<<p.slots, 128, dyn, stream>>>(p);
+        else bt128::sampler_cta_kernel<kModeEpoch, false><<<p.slots, 128, dyn, stream>>>(p);
     } else {
-        if (deterministic) bt256::sampler_cta_kernel<kModeDet><<<p.slots, 256, dyn, stream>>>(p);
-        else bt256::sampler_cta_kernel<kModeEpoch><<<p.slots, 256, dyn, stream>>>(p);
+        if (deterministic) bt256::sampler_cta_kernel<kModeDet, false><<<p.slots, 256, dyn, stream>>>(p);
+        else bt256::sampler_cta_kernel<kModeEpoch, false><<<p.slots, 256, dyn, stream>>>(p);
     }
     ADSB_CUDA(cudaGetLastError());
 }
@@ -117,8 +138,13 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
 void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     configure_once();
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
-    if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused><<<p.slots, 128, dyn, stream>>>(p);
-    else bt256::sampler_cta_kernel<kModeFused><<<p.slots, 256, dyn, stream>>>(p);
+    if (!p.use_smem) {
+        bt256::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 256, 0, stream>>>(p);
+        ADSB_CUDA(cudaGetLastError());
+        return;
+    }
+    if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused, false><<<p.slots, 128, dyn, stream>>>(p);
+    else bt256::sampler_cta_kernel<kModeFused, false><<<p.slots, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
 }
 

@@ -46,6 +46,7 @@ struct Shared {
 // Empty slots have key 0xFFFFFFFF and sigma 0 (sigma is zeroed with the key,
 // so concurrent claimers and adders never race on initialisation).
 struct SmemStore {
+    static constexpr uint32_t kUnrollEdges = ADSB_UNROLL;
     unsigned long long* km;
     unsigned long long* sig;
     uint32_t* qv;      // queue: vertex ids
@@ -150,10 +151,20 @@ struct SmemStore {
     __device__ unsigned long long sigma(uint32_t slot) const { return sig[slot]; }
     __device__ bool queue_ok(uint32_t s_cnt, uint32_t t_cnt) const { return s_cnt + t_cnt <= qcap; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
+    // A one-pass (speculative) level is safe when it cannot claim more vertices
+    // than the table has left: the level claims at most its adjacency count.
+    __device__ bool room_for(unsigned long long edges) const {
+        const uint32_t used = sh->inserted;
+        return used < limit && edges <= limit - used;
+    }
 };
 
 // Per-block dense global state (stamped with a per-block generation tag).
-struct GlobalStore {
+// kU: adjacency loads kept in flight per thread by for_edges (the global-only
+// kernel trades registers for memory-level parallelism).
+template <uint32_t kU>
+struct GlobalStoreT {
+    static constexpr uint32_t kUnrollEdges = kU;
     unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* qdeg;
@@ -195,6 +206,7 @@ struct GlobalStore {
     __device__ unsigned long long sigma(uint32_t slot) const { return __ldcg(st + 2ull * slot + 1); }
     __device__ bool queue_ok(uint32_t, uint32_t) const { return true; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
+    __device__ bool room_for(unsigned long long) const { return true; }
 };
 
 struct Ctx {
@@ -247,7 +259,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         unsigned long long o_val = 0;
         bool have = false;
         // kUnroll adjacency loads in flight per thread before any is consumed
-        constexpr uint32_t kUnroll = ADSB_UNROLL;
+        constexpr uint32_t kUnroll = Store::kUnrollEdges;
         for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kUnroll) {
             uint32_t vv[kUnroll], vs[kUnroll];
             unsigned long long vval[kUnroll];
@@ -318,7 +330,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     uint32_t s_lo = 0, s_hi = 1, t_lo = 0, t_hi = 1, a = 0, b = 0;
     unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
     for (;;) {
-        if (deg_s <= deg_t && Store::kSpeculativeClaims) {
+        if (deg_s <= deg_t && S.room_for(deg_s)) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
             C.verts += C.tid == 0 ? s_hi - s_lo : 0;
@@ -335,9 +347,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.claim(v, a + 1, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
+                              if (Store::kSigmaPreZeroed) S.add_sigma(sl, su);
                               const uint32_t pos = atomicAdd(&sh.s_cnt, 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              ADSB_DCHECK(pos + sh.t_cnt < S.qcap);
+                              ADSB_DCHECK(pos + sh.t_cnt <= S.qcap);
                               S.qv[pos] = v;
                               S.qdeg[pos] = dg;
                               my_deg += dg;
@@ -345,10 +358,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                               if (!(m & kMetaDag)) S.set_dag(sl);
                               met = true;
+                          } else if (Store::kSigmaPreZeroed && !m_is_t(m) && m_dist(m) == a + 1) {
+                              S.add_sigma(sl, su);
                           }
                       });
             if (my_deg) atomicAdd(&sh.degsum, my_deg);
             if (__syncthreads_or(met)) return {a, b, 0};
+            if (!Store::kSigmaPreZeroed)
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -356,12 +372,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.find(v, m);
                           if (sl != kNone && !m_is_t(m) && m_dist(m) == a + 1) S.add_sigma(sl, su);
                       });
+            __syncthreads();  // pre-zeroed stores skip the sigma pass: s_cnt/degsum final here
             s_lo = s_hi;
             s_hi = sh.s_cnt;
             deg_s = sh.degsum;
             a += 1;
             if (s_lo == s_hi) return {a, b, 2};
-        } else if (deg_s > deg_t && Store::kSpeculativeClaims) {
+        } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             C.verts += C.tid == 0 ? t_hi - t_lo : 0;
             bool met = false;
@@ -380,7 +397,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.zero_sigma(sl);
                               const uint32_t j = atomicAdd(&sh.t_cnt, 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              ADSB_DCHECK(j + sh.s_cnt < S.qcap);
+                              ADSB_DCHECK(j + sh.s_cnt <= S.qcap);
                               S.qv[S.tpos(j)] = v;
                               S.qdeg[S.tpos(j)] = dg;
                               my_deg += dg;
@@ -703,17 +720,19 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 
 // One sample (s, t draw + traversal + backtrack) with the shared-memory store
 // first and the global store as fallback. Returns 0 ok or an error code.
-template <int kMode>
-__device__ void one_sample(Ctx& C, SmemStore& sm, GlobalStore& gs, const SamplerParams& p, SplitMix64& rng,
+template <int kMode, bool kGlobalOnly, class GS>
+__device__ void one_sample(Ctx& C, SmemStore& sm, GS& gs, const SamplerParams& p, SplitMix64& rng,
                            uint32_t frame_local, unsigned long long& fallbacks, unsigned long long& errors) {
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
     uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
     if (t >= s) ++t;
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
     int rc = 1;
-    if (p.use_smem) rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+    if constexpr (!kGlobalOnly) {
+        if (p.use_smem) rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+    }
     if (rc == 1) {
-        fallbacks += p.use_smem ? 1 : 0;
+        fallbacks += (!kGlobalOnly && p.use_smem) ? 1 : 0;
         gs.tag += 1;
         rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
     }
@@ -804,8 +823,9 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
     }
 }
 
-template <int kMode>
-__global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_cta_kernel(SamplerParams p) {
+template <int kMode, bool kGlobalOnly>
+__global__ void __launch_bounds__(kBT, (kGlobalOnly ? 2 : ADSB_MINB_PER_256) * 256 / kBT)
+    sampler_cta_kernel(SamplerParams p) {
     extern __shared__ unsigned long long dyn[];
     __shared__ Shared sh;
     Ctx C;
@@ -833,7 +853,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
     sm.level_cap = kSmemLevels;
     sm.sh = &sh;
 
-    GlobalStore gs;
+    GlobalStoreT<kGlobalOnly ? 4 : 1> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.qdeg = reinterpret_cast<uint32_t*>(p.qrange + static_cast<size_t>(p.slot_stride) * slot);
@@ -842,7 +862,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
     gs.qcap = p.n;
     gs.level_cap = p.level_cap;
 
-    sm.clear_all(C.tid);
+    if constexpr (!kGlobalOnly) sm.clear_all(C.tid);
     __syncthreads();
     unsigned long long samples = 0, fallbacks = 0, errors = 0;
     if (kMode != kModeFused) {
@@ -856,7 +876,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
             SplitMix64 rng(reseed(p.seed, p.first + local));
             for (uint64_t i = 0; i < p.spf; ++i) {
                 ++samples;
-                one_sample<kMode>(C, sm, gs, p, rng, static_cast<uint32_t>(local), fallbacks, errors);
+                one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, static_cast<uint32_t>(local), fallbacks, errors);
             }
         }
     } else {
@@ -885,7 +905,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT) sampler_ct
             const uint32_t k = static_cast<uint32_t>((item / p.epoch_b) % p.ring_k);
             SplitMix64 rng(reseed(p.seed, item));
             ++samples;
-            one_sample<kMode>(C, sm, gs, p, rng, k, fallbacks, errors);
+            one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, k, fallbacks, errors);
             if (C.tid == 0) {
                 __threadfence();  // this sample's counts before its completion
                 sh.flag = atomicAdd(p.ctl + kCtlDone + k, 1ull) + 1 == p.epoch_b ? 1u : 0u;
