@@ -108,6 +108,7 @@ struct DeviceGraph {
     int device = 0;
     uint32_t n = 0;
     uint64_t nnz = 0;
+    uint32_t max_degree = 0;
     DevBuf<uint32_t> offsets;  // n+1 (nnz < 2^32 on the device path)
     DevBuf<uint32_t> nbrs;     // nnz
 };

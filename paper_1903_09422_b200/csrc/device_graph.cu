@@ -213,6 +213,7 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
     // u32 offsets on the device: narrow on the host, then one copy each.
     std::vector<uint32_t> off32(g.offsets.size());
     for (size_t i = 0; i < off32.size(); ++i) off32[i] = static_cast<uint32_t>(g.offsets[i]);
+    for (uint32_t u = 0; u < g.n; ++u) dg.max_degree = std::max<uint32_t>(dg.max_degree, off32[u + 1] - off32[u]);
     dg.offsets = take_buffer(*ctx->rt, off32.size());
     dg.nbrs = take_buffer(*ctx->rt, std::max<uint64_t>(1, g.nnz()));
     ctx->labels = take_buffer(*ctx->rt, std::max<uint32_t>(1, g.n));

@@ -230,6 +230,7 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.label = ctx.labels.ptr;
     p.n = ctx.graph.n;
     p.slot_stride = a.n;
+    p.max_degree = std::getenv("ADSB_NO_LOWDEG") ? 0xFFFFFFFFu : ctx.graph.max_degree;
     p.slots = a.slots;
     p.level_cap = a.level_cap;
     p.rank = 0;

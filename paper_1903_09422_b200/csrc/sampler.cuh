@@ -57,6 +57,7 @@ struct SamplerParams {
     uint32_t use_smem;     // block sampler: try the shared-memory store first
     uint32_t block_threads; // block sampler: 128 or 256
     uint32_t global_grid;   // block sampler: resident blocks of the global-store-only variant
+    uint32_t max_degree;    // graph max degree (low-degree graphs use thread-per-vertex expansion)
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode

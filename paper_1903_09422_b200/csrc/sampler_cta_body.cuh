@@ -10,6 +10,7 @@ constexpr uint32_t kMetaT = 1u << 31;
 constexpr uint32_t kMetaDag = 1u << 30;
 constexpr uint32_t kMetaDist = (1u << 30) - 1;
 constexpr uint32_t kSmemLevels = 64;
+constexpr uint32_t kSmallStep = 64;  // backtrack steps with deg(cur) <= this run on warp 0 alone
 
 __device__ __forceinline__ bool m_is_t(uint32_t m) { return (m & kMetaT) != 0; }
 __device__ __forceinline__ uint32_t m_dist(uint32_t m) { return m & kMetaDist; }
@@ -218,6 +219,7 @@ struct Ctx {
     Shared* sh;
     unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
     uint32_t n;
+    bool low_degree;
 };
 
 // Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
@@ -227,6 +229,26 @@ template <class Store, class Prep, class Body>
 __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long& counter,
                           Prep prep, Body body) {
     Shared& sh = *C.sh;
+    if (C.low_degree) {
+        // Low-degree graphs (max degree <= 32, e.g. the grid): one thread per
+        // frontier vertex walks its whole adjacency; no scan, no chunk
+        // barriers, one barrier per level. Imbalance is bounded by the max degree.
+        unsigned long long mine = 0;
+        for (uint32_t i = lo + C.tid; i < hi; i += kBT) {
+            const uint32_t q = t_list ? S.tpos(i) : i;
+            const uint32_t u = S.qv[q];
+            ADSB_DCHECK(u < C.n);
+            const uint32_t o = C.off[u], e = C.off[u + 1];
+            uint32_t meta;
+            const uint32_t slot = S.find(u, meta);
+            const unsigned long long val = prep(slot, meta, e - o);
+            mine += e - o;
+            for (uint32_t j = o; j < e; ++j) body(slot, val, C.nbrs[j]);
+        }
+        counter += mine;
+        __syncthreads();
+        return;
+    }
     for (uint32_t base = lo; base < hi; base += kBT) {
         const uint32_t i = base + C.tid;
         uint32_t deg = 0, o = 0, slot = 0;
@@ -591,7 +613,71 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         }
         const uint32_t beg = C.off[cur], end = C.off[cur + 1];
         bool found = false;
-        for (uint32_t base = beg; base < end; base += kBT) {
+        if (end - beg <= kSmallStep) {
+            // Low-degree step: warp 0 scans alone (warp-level 65-bit prefix),
+            // one barrier publishes the choice; saves the block-wide rounds.
+            if (C.warp == 0) {
+                uint32_t ch = kNone, chm = 0, first = kNone, firstm = 0;
+                unsigned long long chs = 0;
+                for (uint32_t base = beg; base < end && ch == kNone; base += 32) {
+                    const uint32_t i = base + C.lane;
+                    uint32_t q = 0, m = 0;
+                    unsigned long long val = 0;
+                    bool cand = false;
+                    if (i < end) {
+                        q = C.nbrs[i];
+                        const uint32_t sl = S.find(q, m);
+                        cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist &&
+                               (!want_t || (m & kMetaDag));
+                        if (cand) val = S.sigma(sl);
+                    }
+                    C.back_edges += C.lane == 0 ? min(32u, end - base) : 0;
+                    const uint32_t cb = __ballot_sync(kFull, cand);
+                    if (first == kNone && cb) {
+                        const int f0 = __ffs(cb) - 1;
+                        first = __shfl_sync(kFull, q, f0);
+                        firstm = __shfl_sync(kFull, m, f0);
+                    }
+                    unsigned long long lo = val;
+                    uint32_t hi = 0;
+#pragma unroll
+                    for (int dd = 1; dd < 32; dd <<= 1) {
+                        const unsigned long long olo = __shfl_up_sync(kFull, lo, dd);
+                        const uint32_t ohi = __shfl_up_sync(kFull, hi, dd);
+                        if (C.lane >= static_cast<uint32_t>(dd)) add65(lo, hi, olo, ohi);
+                    }
+                    const uint32_t ball = __ballot_sync(kFull, hi > 0 || r < lo);
+                    if (ball) {
+                        const int f = __ffs(ball) - 1;
+                        ch = __shfl_sync(kFull, q, f);
+                        chm = __shfl_sync(kFull, m, f);
+                        chs = __shfl_sync(kFull, val, f);
+                    } else {
+                        r -= __shfl_sync(kFull, lo, 31);
+                    }
+                }
+                if (ch == kNone && first != kNone) {  // degenerate sigma (see the block path)
+                    ch = first;
+                    chm = firstm;
+                    chs = 0;
+                    C.degenerate += C.lane == 0 ? 1 : 0;
+                }
+                if (C.lane == 0) {
+                    sh.first = ch;
+                    sh.ch = ch;
+                    sh.chm = chm;
+                    sh.chs = chs;
+                }
+            }
+            __syncthreads();
+            found = sh.first != kNone;
+            cur = sh.ch;
+            cmeta = sh.chm;
+            csig = sh.chs;
+            __syncthreads();
+            if (!found) return false;
+        }
+        for (uint32_t base = beg; !found && base < end; base += kBT) {
             const uint32_t i = base + C.tid;
             uint32_t q = 0, m = 0;
             unsigned long long val = 0;
@@ -824,7 +910,7 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
 }
 
 template <int kMode, bool kGlobalOnly>
-__global__ void __launch_bounds__(kBT, (kGlobalOnly ? 2 : ADSB_MINB_PER_256) * 256 / kBT)
+__global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     sampler_cta_kernel(SamplerParams p) {
     extern __shared__ unsigned long long dyn[];
     __shared__ Shared sh;
@@ -837,6 +923,7 @@ __global__ void __launch_bounds__(kBT, (kGlobalOnly ? 2 : ADSB_MINB_PER_256) * 2
     C.sh = &sh;
     C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
     C.n = p.n;
+    C.low_degree = p.max_degree <= 32;
     const uint32_t slot = blockIdx.x;
 
     SmemStore sm;
@@ -853,7 +940,7 @@ __global__ void __launch_bounds__(kBT, (kGlobalOnly ? 2 : ADSB_MINB_PER_256) * 2
     sm.level_cap = kSmemLevels;
     sm.sh = &sh;
 
-    GlobalStoreT<kGlobalOnly ? 4 : 1> gs;
+    GlobalStoreT<1> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.qdeg = reinterpret_cast<uint32_t*>(p.qrange + static_cast<size_t>(p.slot_stride) * slot);

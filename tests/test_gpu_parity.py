@@ -150,12 +150,10 @@ def test_sampler_variants_bit_exact(mode, monkeypatch, grid200):
     """All sampler implementations (block teams with the shared-memory table,
     block teams forced onto global state, a table so small that most samples
     overflow and are redone, warp teams) give the same paths and results."""
-    monkeypatch.delenv("ADSB_SAMPLER", raising=False)
     monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
     monkeypatch.delenv("ADSB_HASH_CAP", raising=False)
-    if mode == "warp":
-        monkeypatch.setenv("ADSB_SAMPLER", "warp")
-    elif mode == "block-global":
+    monkeypatch.setenv("ADSB_SAMPLER", "warp" if mode == "warp" else "block")  # small n would pick warps
+    if mode == "block-global":
         monkeypatch.setenv("ADSB_NO_SMEM", "1")
     elif mode == "block-tinyhash":
         monkeypatch.setenv("ADSB_HASH_CAP", "64")
@@ -249,3 +247,29 @@ def test_epoch_block_teams_fused_and_host_driven(fused, B, monkeypatch):
     cap = EngineConfig(variant=Variant.shared, threads=4, base_seed=13, epoch_samples=B, max_cycles=3)
     r = estimate_bc(pg.graph, 0.01, 0.1, cap)
     assert r.tau == 3 * B and r.reason.name == "capped"
+
+
+@pytest.mark.parametrize("mode", ["block", "block-global", "block-128"])
+@pytest.mark.parametrize("spf", [1, 4])
+def test_block_teams_frames_ba(mode, spf, monkeypatch):
+    """Block teams on a hub-heavy BA graph (shared-memory table overflows for
+    some samples and falls back), including spf > 1 (stream continuity across
+    samples of one frame)."""
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    monkeypatch.delenv("ADSB_BLOCK", raising=False)
+    if mode == "block-global":
+        monkeypatch.setenv("ADSB_NO_SMEM", "1")
+    elif mode == "block-128":
+        monkeypatch.setenv("ADSB_BLOCK", "128")
+    p = datasets.gen_ba(1 << 15, 8, 3)
+    pg, og = both(p)
+    got = sample_frames(pg.graph, 21, spf, 5, 300)
+    want = oracle.sample_frames(og, 21, spf, 5, 300)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=spf, base_seed=21, threads=4, max_cycles=600)
+    r = estimate_bc(pg.graph, 0.02, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.02, 0.1, spf=spf, seed=21, nominal_threads=4, max_frames=600)
+    assert (r.tau, r.run.check_cycles, r.reason.name) == (o.tau, o.check_cycles, o.reason)
+    np.testing.assert_array_equal(r.run.data, o.counts)
