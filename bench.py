@@ -173,6 +173,23 @@ def cpu_baseline(w, path) -> dict:
     return {"value": None, "unit": "samples/s", "cores": cores, "kind": "reference", "sample": "ref_driver absent"}
 
 
+REF_EQUIV_SAMPLES = {"c1_er": 400, "c2_rmat18": 40, "c3_ba": 10, "c4_grid": 10, "c5_rmat24": 2}
+
+
+def reference_equivalent(w, value: float) -> dict:
+    """Bytes the reference's forward BFS (kadabra.hpp:208-242) reads per sample,
+    replayed by the oracle on a few samples of the same graph and seed."""
+    import oracle
+    from paper_1903_09422_b200 import datasets
+    k = REF_EQUIV_SAMPLES.get(w.name, 10)
+    g = oracle.from_pairs(datasets.pairs(w.name))
+    r = oracle.estimate_bc(g, w.epsilon, w.delta, spf=1, seed=w.seed, max_frames=k)
+    per = (4 * r.edges_scanned + 8 * r.vertices_expanded) / max(1, r.tau)
+    return {"forward_bfs_bytes_per_sample": per, "samples_replayed": r.tau,
+            "equivalent_gbs": per * value / 1e9,
+            "note": "edge-read rate the reference algorithm would need for the same samples/s"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -326,6 +343,11 @@ def main() -> None:
     }
     if e2e:
         line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline and g.num_edges() <= 50_000_000:
+        try:
+            line["reference_equivalent"] = reference_equivalent(w, value)
+        except Exception as e:  # pragma: no cover
+            line["reference_equivalent"] = {"error": str(e)}
     if world == 1 and not args.no_cpu_baseline:
         if g.num_edges() > 50_000_000 and not args.force_cpu_baseline:
             line["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",

@@ -289,6 +289,30 @@ uint64_t run_det_batch(DeviceContext& ctx, SamplerParams p, unsigned long long*&
     }
 }
 
+// Frames still needed before the rule can pass, predicting that the largest
+// count keeps growing in proportion to tau (b = max_count / tau stays fixed):
+// the smallest tau with f(b) <= eps and g(b) <= eps (both decrease in tau at
+// fixed b), found by bisection with the host formulas. Used only to size
+// batches; the stop itself is decided exactly by the ordered cutoff.
+uint64_t predict_stop_tau(uint64_t max_count, uint64_t tau, uint64_t omega, double eps, double log_inv) {
+    if (tau == 0) return omega;
+    const double b = static_cast<double>(max_count) / static_cast<double>(tau);
+    auto pass = [&](uint64_t t) {
+        if (t >= omega) return true;
+        const double td = static_cast<double>(t);
+        return f_kernel(b, log_inv, static_cast<double>(omega), td) <= eps &&
+               g_kernel(b, log_inv, static_cast<double>(omega), td) <= eps;
+    };
+    uint64_t lo = tau, hi = omega;
+    if (pass(lo)) return lo;
+    while (lo + 1 < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (pass(mid)) hi = mid;
+        else lo = mid;
+    }
+    return hi;
+}
+
 bool trace_enabled() {
     static const bool on = std::getenv("ADSB_TRACE") != nullptr;
     return on;
@@ -352,7 +376,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     // work units that keep every team busy: warps are many and light, blocks few and heavy
     const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).slots;
 
-    if (opt.deterministic && !opt.comm && !std::getenv("ADSB_NO_DET_PIPELINE")) {
+    if (opt.deterministic && !opt.comm && std::getenv("ADSB_DET_PIPELINE")) {
         // ---- deterministic frames, pipelined: while the host reads batch b's
         // event count and stream 2 runs its ordered cutoff, stream 1 already
         // samples batch b+1 (speculatively; wasted if b stops). Two event
@@ -529,8 +553,19 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         uint64_t sampled_frames = 0;
         bool stopped = false;
         uint32_t stop_local = kNoStop;
+        uint64_t cur_max = 0;  // largest count after the frames folded so far
         while (!stopped) {
-            uint64_t F = std::max<uint64_t>(2 * team_slots * world, done);
+            // Batch size: the predicted remaining frames (+5%), at least a few
+            // frames per team; the first batch has no prediction yet.
+            uint64_t F = 2 * team_slots * world;
+            if (done > 0) {
+                const uint64_t tau_star = predict_stop_tau(cur_max, done * spf, out.omega, eps, log_inv);
+                const uint64_t need = (tau_star > done * spf ? (tau_star - done * spf + spf - 1) / spf : 1);
+                // never more than the doubling schedule: early max counts are
+                // biased high, so the prediction overshoots then
+                F = std::min<uint64_t>(std::max<uint64_t>(need + need / 20 + 1, team_slots * world / 2),
+                                       std::max<uint64_t>(done, F));
+            }
             F = std::min<uint64_t>(F, frame_limit - done);
             F = std::min<uint64_t>(F, 1ull << 30);
             SamplerParams p = base_params(ctx, opt.seed, spf);
@@ -590,9 +625,11 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             k_find_stop<<<grid_for(F, ctx.device), 256, 0, s1>>>(run_max, static_cast<uint32_t>(F), base_max, done, spf,
                                                                  rule, stop_idx);
             ADSB_CUDA(cudaMemcpyAsync(stop_h, stop_idx, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
+            ADSB_CUDA(cudaMemcpyAsync(stop_h + 1, run_max + (F - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
             ADSB_CUDA(cudaStreamSynchronize(s1));
             L.count += 3;
             const uint32_t stop_host = *stop_h;
+            cur_max = std::max<uint64_t>(cur_max, stop_h[1]);
             uint32_t limit = static_cast<uint32_t>(F - 1);
             if (stop_host != kNoStop) {
                 limit = stop_host;
