@@ -7,9 +7,11 @@ which mirror the reference's exception types (include/adsb.h header comment).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libadsb.so"
+# ADSB_LIB_PATH: load another in-tree build (A/B comparisons of kernel changes)
+LIB_PATH = Path(os.environ.get("ADSB_LIB_PATH") or Path(__file__).resolve().parent / "libadsb.so")
 
 
 class AdsbError(RuntimeError):

@@ -25,13 +25,18 @@ namespace {
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 
+// Parent pointers only ever decrease (hooks link the larger root below the
+// smaller; halving skips to a smaller ancestor). Every pointer write is an
+// atomicMin so a thread holding a stale read can never raise one again: with
+// plain stores, a late halving write could overwrite uf_compress's
+// parent[v] = root with a non-root ancestor and mislabel v.
 __device__ __forceinline__ uint32_t uf_root(uint32_t* parent, uint32_t v) {
     volatile uint32_t* p = parent;
     uint32_t cur = p[v];
     if (cur != v) {
         uint32_t prev = v, next;
-        while (cur > (next = p[cur])) {  // path halving; parents only decrease
-            p[prev] = next;
+        while (cur > (next = p[cur])) {  // path halving
+            atomicMin(parent + prev, next);
             prev = cur;
             cur = next;
         }
@@ -69,8 +74,8 @@ __global__ void uf_hook(const uint32_t* __restrict__ off, const uint32_t* __rest
 
 __global__ void uf_compress(uint32_t* parent, uint32_t* is_root, uint32_t n) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const uint32_t r = uf_root(parent, v);
-        parent[v] = r;
+        const uint32_t r = uf_root(parent, v);  // hooking is complete: r is final
+        atomicMin(parent + v, r);
         is_root[v] = r == v ? 1u : 0u;
     }
 }

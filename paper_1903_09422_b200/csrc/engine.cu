@@ -684,6 +684,14 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         p.max_epochs = max_epochs;
         p.ring_k = K;
         p.rule = rule;
+        // ADSB_FUSED_AUDIT=<file>: per sample (ticket) the increments it recorded
+        // | its distance << 16, then per epoch the increments folds consumed:
+        // u32[max_epochs * B + max_epochs] (diagnostics only)
+        const char* audit_path = std::getenv("ADSB_FUSED_AUDIT");
+        if (audit_path) {
+            p.audit = ctx.rt->pool.get<uint32_t>(Scratch::kAudit, (B + 1) * max_epochs);
+            ADSB_CUDA(cudaMemsetAsync(p.audit, 0, (B + 1) * max_epochs * sizeof(uint32_t), s1));
+        }
         ADSB_CUDA(cudaEventRecord(e0, s1));
         launch_sampler_fused(p, s1);
         ADSB_CUDA(cudaEventRecord(e1, s1));
@@ -703,6 +711,14 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         ADSB_CUDA(cudaMemcpyAsync(ctl_h + 8, stats + kStatSamples, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
         ADSB_CUDA(cudaStreamSynchronize(s1));
         out.total_samples = ctl_h[8];
+        if (audit_path) {
+            std::vector<uint32_t> a((B + 1) * max_epochs);
+            ADSB_CUDA(cudaMemcpy(a.data(), p.audit, a.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            if (FILE* f = std::fopen(audit_path, "wb")) {
+                std::fwrite(a.data(), sizeof(uint32_t), a.size(), f);
+                std::fclose(f);
+            }
+        }
         if (trace_enabled())
             std::fprintf(stderr, "[adsb] fused epochs: B %llu stop epoch %llu drawn %llu t=%.3f ms\n",
                          static_cast<unsigned long long>(B), static_cast<unsigned long long>(stop),

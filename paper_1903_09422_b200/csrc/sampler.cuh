@@ -87,6 +87,7 @@ struct SamplerParams {
     uint64_t epoch_b;
     uint64_t max_epochs;
     uint32_t ring_k;
+    uint32_t* audit;  // fused diagnostics (ADSB_FUSED_AUDIT): [epoch] recorded, [max_epochs + epoch] folded
     RuleParams rule;
 };
 

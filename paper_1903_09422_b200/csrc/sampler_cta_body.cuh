@@ -24,7 +24,7 @@ struct Shared {
     uint32_t cslot[kBT];              // store slot of the chunk's frontier vertex
     unsigned long long cval[kBT];     // per-vertex payload (sigma of u)
     unsigned long long item;
-    unsigned long long degsum;
+    uint32_t degsum;                  // adjacency total of the level being claimed (< 2^32: u32 offsets)
     uint32_t s_cnt, t_cnt;            // queue fill: s-side from 0 up, t-side from the top down
     uint32_t inserted;                // hash reservations this sample
     uint32_t overflow;
@@ -34,6 +34,8 @@ struct Shared {
     uint32_t first;                   // backtrack: first thread whose prefix exceeds r
     uint32_t ch, chm;                 // backtrack: chosen predecessor and its meta
     unsigned long long chs;           // backtrack: chosen predecessor's sigma
+    uint32_t bch, bchm;               // backtrack, block rounds: chosen predecessor and meta
+    unsigned long long bchs;          //   and its sigma
     unsigned long long ev_pos;
     unsigned long long fold_epoch;    // fused mode: epoch being folded
     uint32_t fold_len, fold_max, flag;
@@ -69,7 +71,12 @@ struct SmemStore {
             sig[i] = 0ull;
         }
     }
-    __device__ void begin(uint32_t) {}
+    __device__ void begin(uint32_t tid) {
+#ifdef ADSB_DEBUG_CHECKS
+        for (uint32_t i = tid; i <= mask; i += kBT)
+            ADSB_DCHECK(km[i] == ~0ull && sig[i] == 0ull, "hash table not clean at sample start");
+#endif
+    }
     // Reset exactly the slots this sample inserted (the queue lists them) so
     // the next sample starts from an empty table without touching all of it.
     template <class CtxT>
@@ -147,8 +154,23 @@ struct SmemStore {
     static constexpr bool kSigmaPreZeroed = true;  // claim and sigma accumulation share one pass
     static constexpr bool kSpeculativeClaims = false;  // meeting-level claims would overflow the table
     __device__ void zero_sigma(uint32_t) {}
-    __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(&sig[slot], x); }
-    __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], static_cast<unsigned long long>(kMetaDag)); }
+    // 64-bit shared-memory atomics are CAS loops on sm_100; sigma (mod 2^64)
+    // is added as two native 32-bit atomics with the carry of the low word
+    // (each wrap of the low word is seen by exactly one adder). Sigma is only
+    // read after a barrier, never while adds are in flight.
+    __device__ void add_sigma(uint32_t slot, unsigned long long x) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(&sig[slot]);
+        const uint32_t xl = static_cast<uint32_t>(x), xh = static_cast<uint32_t>(x >> 32);
+        uint32_t carry = 0;
+        if (xl) {
+            const uint32_t old = atomicAdd(w, xl);
+            carry = old + xl < old ? 1u : 0u;
+        }
+        if (xh | carry) atomicAdd(w + 1, xh + carry);
+    }
+    // the meta half (low word) of key << 32 | meta; no claim CASes a slot that
+    // already holds a key, so the 32-bit OR never overlaps a 64-bit CAS
+    __device__ void set_dag(uint32_t slot) { atomicOr(reinterpret_cast<uint32_t*>(&km[slot]), kMetaDag); }
     __device__ unsigned long long sigma(uint32_t slot) const { return sig[slot]; }
     __device__ bool queue_ok(uint32_t s_cnt, uint32_t t_cnt) const { return s_cnt + t_cnt <= qcap; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
@@ -218,6 +240,8 @@ struct Ctx {
     uint32_t warp;
     Shared* sh;
     unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
+    uint32_t recorded;  // increments recorded by this thread (thread 0 records)
+    uint32_t last_d;    // distance of the last sample (diagnostics)
     uint32_t n;
     bool low_degree;
 };
@@ -322,6 +346,12 @@ __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int s
     return __shfl_sync(kFull, x, src);
 }
 
+// One shared atomic per warp for the level's adjacency total.
+__device__ __forceinline__ void add_degsum(Ctx& C, uint32_t my_deg) {
+    const uint32_t w = __reduce_add_sync(kFull, my_deg);
+    if (C.lane == 0 && w) atomicAdd(&C.sh->degsum, w);
+}
+
 // Result of the BFS phase: distance split d = a + b + 1.
 struct Meet {
     uint32_t a, b;
@@ -360,7 +390,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             __syncthreads();  // every thread has read the previous level's degsum
             if (C.tid == 0) sh.degsum = 0;
             __syncthreads();
-            unsigned long long my_deg = 0;
+            uint32_t my_deg = 0;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -384,7 +414,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                           }
                       });
-            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            add_degsum(C, my_deg);
             if (__syncthreads_or(met)) return {a, b, 0};
             if (!Store::kSigmaPreZeroed)
             for_edges(C, S, s_lo, s_hi, false, C.edges,
@@ -407,7 +437,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             __syncthreads();  // every thread has read the previous level's degsum
             if (C.tid == 0) sh.degsum = 0;
             __syncthreads();
-            unsigned long long my_deg = 0;
+            uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -429,7 +459,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               met = true;
                           }
                       });
-            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            add_degsum(C, my_deg);
             if (__syncthreads_or(met)) return {a, b, 0};
             t_lo = t_hi;
             t_hi = sh.t_cnt;
@@ -459,7 +489,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- no meeting: claim level a+1, then accumulate its sigma
             if (C.tid == 0) sh.degsum = 0;
             __syncthreads();
-            unsigned long long my_deg = 0;
+            uint32_t my_deg = 0;
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return Store::kSigmaPreZeroed ? S.sigma(slot) : 0ull; },
@@ -482,7 +512,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               my_deg += dg;
                           }
                       });
-            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            add_degsum(C, my_deg);
             __syncthreads();  // degsum complete before any thread reads it (uniform side choice)
             if (sh.overflow) return {a, b, 1};
             if (!Store::kSigmaPreZeroed)
@@ -516,7 +546,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (__syncthreads_or(met)) return {a, b, 0};
             if (C.tid == 0) sh.degsum = 0;
             __syncthreads();
-            unsigned long long my_deg = 0;
+            uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -537,7 +567,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               my_deg += dg;
                           }
                       });
-            if (my_deg) atomicAdd(&sh.degsum, my_deg);
+            add_degsum(C, my_deg);
             __syncthreads();
             if (sh.overflow) return {a, b, 1};
             t_lo = t_hi;
@@ -576,6 +606,19 @@ __device__ __forceinline__ void add65(unsigned long long& lo, uint32_t& hi, unsi
     lo = n;
 }
 
+// First lane (in lane order) among the candidates `cb` at which the running
+// `r -= val` scan stops (r < val), or -1 with r reduced by the chunk's total.
+// Warp-uniform; cost is one 64-bit shuffle per candidate.
+__device__ __forceinline__ int pick_candidate(uint32_t cb, unsigned long long val, unsigned long long& r) {
+    for (uint32_t bits = cb; bits; bits &= bits - 1) {
+        const int j = __ffs(bits) - 1;
+        const unsigned long long x = __shfl_sync(kFull, val, j);
+        if (r < x) return j;
+        r -= x;
+    }
+    return -1;
+}
+
 // Block-wide backtrack (kadabra.hpp:227-242). Every step scans N(cur) in
 // ascending order, kBT entries per round: each thread tests one neighbour
 // against the predecessor rule, a 65-bit block prefix sum over the
@@ -590,6 +633,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
     Shared& sh = *C.sh;
     constexpr uint32_t kNW = kBT / 32;
     const uint32_t d = mt.a + mt.b + 1;
+    C.last_d = d;
     if (d < 2) return true;
     constexpr bool kDet = kMode == kModeDet;
     if (kDet && C.tid == 0) sh.ev_pos = atomicAdd(p.ev_cursor, static_cast<unsigned long long>(d - 1));
@@ -638,22 +682,13 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                         first = __shfl_sync(kFull, q, f0);
                         firstm = __shfl_sync(kFull, m, f0);
                     }
-                    unsigned long long lo = val;
-                    uint32_t hi = 0;
-#pragma unroll
-                    for (int dd = 1; dd < 32; dd <<= 1) {
-                        const unsigned long long olo = __shfl_up_sync(kFull, lo, dd);
-                        const uint32_t ohi = __shfl_up_sync(kFull, hi, dd);
-                        if (C.lane >= static_cast<uint32_t>(dd)) add65(lo, hi, olo, ohi);
-                    }
-                    const uint32_t ball = __ballot_sync(kFull, hi > 0 || r < lo);
-                    if (ball) {
-                        const int f = __ffs(ball) - 1;
+                    // the reference's sequential `r -= sigma[p]` over this
+                    // chunk's predecessors, in id (= lane) order
+                    const int f = pick_candidate(cb, val, r);
+                    if (f >= 0) {
                         ch = __shfl_sync(kFull, q, f);
                         chm = __shfl_sync(kFull, m, f);
                         chs = __shfl_sync(kFull, val, f);
-                    } else {
-                        r -= __shfl_sync(kFull, lo, 31);
                     }
                 }
                 if (ch == kNone && first != kNone) {  // degenerate sigma (see the block path)
@@ -688,46 +723,58 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                     val = S.sigma(sl);
             }
             C.back_edges += C.tid == 0 ? min(static_cast<uint32_t>(kBT), end - base) : 0;
-            unsigned long long lo = val;
-            uint32_t hi = 0;
+            // per-warp 65-bit candidate totals, then the warp whose range holds
+            // r walks its candidates in lane (= id) order
+            const uint32_t cb = __ballot_sync(kFull, val != 0);
+            unsigned long long wlo = 0;
+            uint32_t whi = 0;
+            if (__popc(cb) <= 4) {
+                for (uint32_t bits = cb; bits; bits &= bits - 1)
+                    add65(wlo, whi, __shfl_sync(kFull, val, __ffs(bits) - 1), 0u);
+            } else {
+                wlo = val;
 #pragma unroll
-            for (int dd = 1; dd < 32; dd <<= 1) {
-                const unsigned long long olo = __shfl_up_sync(kFull, lo, dd);
-                const uint32_t ohi = __shfl_up_sync(kFull, hi, dd);
-                if (C.lane >= static_cast<uint32_t>(dd)) add65(lo, hi, olo, ohi);
+                for (int dd = 16; dd >= 1; dd >>= 1)
+                    add65(wlo, whi, __shfl_xor_sync(kFull, wlo, dd), __shfl_xor_sync(kFull, whi, dd));
             }
-            if (C.lane == 31) {
-                sh.wlo[C.warp] = lo;
-                sh.whi[C.warp] = hi;
+            if (C.lane == 0) {
+                sh.wlo[C.warp] = wlo;
+                sh.whi[C.warp] = whi;
             }
-            if (C.tid == 0) sh.first = kNone;
             __syncthreads();
-            unsigned long long tot_lo = 0;
-            uint32_t tot_hi = 0;
+            unsigned long long pre_lo = 0, tot_lo = 0;
+            uint32_t pre_hi = 0, tot_hi = 0;
             for (uint32_t w = 0; w < kNW; ++w) {
-                if (w == C.warp) add65(lo, hi, tot_lo, tot_hi);  // inclusive block prefix
+                if (w == C.warp) {
+                    pre_lo = tot_lo;
+                    pre_hi = tot_hi;
+                }
                 add65(tot_lo, tot_hi, sh.wlo[w], sh.whi[w]);
             }
-            const uint32_t ball = __ballot_sync(kFull, hi > 0 || r < lo);
-            if (ball && C.lane == static_cast<uint32_t>(__ffs(ball) - 1)) atomicMin(&sh.first, C.tid);
-            __syncthreads();
-            const uint32_t f = sh.first;
-            if (f != kNone) {
-                if (C.tid == f) {
-                    sh.ch = q;
-                    sh.chm = m;
-                    sh.chs = val;
+            // r in [pre, pre + wtot) for exactly one warp when the round holds the choice
+            unsigned long long end_lo = pre_lo;
+            uint32_t end_hi = pre_hi;
+            add65(end_lo, end_hi, wlo, whi);
+            if (pre_hi == 0 && pre_lo <= r && (end_hi > 0 || r < end_lo)) {
+                unsigned long long rr = r - pre_lo;
+                const int f = pick_candidate(cb, val, rr);
+                if (C.lane == static_cast<uint32_t>(f)) {
+                    sh.bch = q;
+                    sh.bchm = m;
+                    sh.bchs = val;
                 }
-                __syncthreads();
-                cur = sh.ch;
-                cmeta = sh.chm;
-                csig = sh.chs;
+            }
+            __syncthreads();
+            if (tot_hi > 0 || r < tot_lo) {
+                // written again only after a later round's first barrier (the
+                // warp-0 path has its own copy), so no trailing barrier
+                cur = sh.bch;
+                cmeta = sh.bchm;
+                csig = sh.bchs;
                 found = true;
-                __syncthreads();
                 break;
             }
-            r -= tot_lo;  // tot_hi == 0 here: otherwise some prefix would exceed r
-            __syncthreads();
+            r -= tot_lo;  // tot_hi == 0 here: otherwise the round would hold the choice
         }
         if (!found) {
             // sigma(cur) and every predecessor sigma are 0 mod 2^64: reference UB
@@ -771,6 +818,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                 atomicAdd(p.counts + cur, 1u);
             } else {
                 // fused: frame_local is the ring slot; record first touches for the fold
+                ++C.recorded;
                 const size_t base = static_cast<size_t>(frame_local) * p.n;
                 if (atomicAdd(p.ring_cnt + base + cur, 1u) == 0u)
                     p.ring_list[base + atomicAdd(p.ring_len + frame_local, 1u)] = cur;
@@ -794,6 +842,13 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
     }
     __syncthreads();
     const Meet mt = bfs(C, S, s, t);
+#ifdef ADSB_DEBUG_CHECKS
+    if (mt.status == 0 && mt.a + mt.b == 0 && C.tid == 0) {
+        bool adj = false;
+        for (uint32_t j = C.off[s]; j < C.off[s + 1]; ++j) adj |= C.nbrs[j] == t;
+        ADSB_DCHECK(adj, "met at distance 1 but t is not a neighbour of s");
+    }
+#endif
     if (mt.status != 0) {
         S.end(C, *C.sh);
         return mt.status;
@@ -812,6 +867,7 @@ __device__ void one_sample(Ctx& C, SmemStore& sm, GS& gs, const SamplerParams& p
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
     uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
     if (t >= s) ++t;
+    C.last_d = 0xFFFF;
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
     int rc = 1;
     if constexpr (!kGlobalOnly) {
@@ -866,15 +922,22 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
             const uint32_t k = static_cast<uint32_t>(f % p.ring_k);
             uint32_t* cnt = p.ring_cnt + static_cast<size_t>(k) * p.n;
             const uint32_t* list = p.ring_list + static_cast<size_t>(k) * p.n;
-            uint32_t local = 0;
+            uint32_t local = 0, consumed = 0;
             for (uint32_t j = C.tid; j < len; j += kBT) {
                 const uint32_t v = __ldcg(list + j);
                 const uint32_t c = atomicExch(cnt + v, 0u);
+                consumed += c;
                 const uint32_t tot = __ldcg(p.total + v) + c;
                 __stcg(p.total + v, tot);
                 local = max(local, tot);
             }
             if (local) atomicMax(&sh.fold_max, local);
+            if (p.audit && consumed) atomicAdd(p.audit + p.max_epochs * p.epoch_b + f, consumed);
+            // Every thread's total[] stores must reach L2 before thread 0
+            // publishes the fold (a fence orders only its own thread's
+            // accesses): otherwise the next lock holder can read a stale total
+            // and overwrite it, losing this epoch's counts.
+            __threadfence();
             __syncthreads();
             if (C.tid == 0) {
                 const unsigned long long m = max(vload(ctl + kCtlMax), static_cast<unsigned long long>(sh.fold_max));
@@ -922,6 +985,8 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
     C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
+    C.recorded = 0;
+    C.last_d = 0;
     C.n = p.n;
     C.low_degree = p.max_degree <= 32;
     const uint32_t slot = blockIdx.x;
@@ -992,8 +1057,11 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
             const uint32_t k = static_cast<uint32_t>((item / p.epoch_b) % p.ring_k);
             SplitMix64 rng(reseed(p.seed, item));
             ++samples;
+            const uint32_t rec0 = C.recorded;
             one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, k, fallbacks, errors);
             if (C.tid == 0) {
+                if (p.audit && item < p.max_epochs * p.epoch_b)
+                    p.audit[item] = (C.recorded - rec0) | (C.last_d << 16);
                 __threadfence();  // this sample's counts before its completion
                 sh.flag = atomicAdd(p.ctl + kCtlDone + k, 1ull) + 1 == p.epoch_b ? 1u : 0u;
             }

@@ -47,6 +47,19 @@ def test_components_and_dub(name):
         assert adsamp.eccentricity(pg.graph, s) == oracle.eccentricity(og, s)
 
 
+def test_components_labels_stable_over_many_builds():
+    """Regression: union-find path halving once raced with uf_compress and
+    mislabelled about one vertex in a thousand builds (samples touching it were
+    dropped as disconnected pairs). Fresh handles recompute the labels."""
+    cases = [datasets.pairs("c1_er"), datasets.gen_gnm(6000, 4000, 5, lcc=False)]  # connected; many components
+    for pairs in cases:
+        lab, comps = oracle.components(oracle.from_pairs(pairs))
+        for _ in range(150):
+            cc = adsamp.connected_components(adsamp.graph_from_pairs(pairs).graph)
+            assert cc.num_components == comps
+            np.testing.assert_array_equal(cc.label, lab)
+
+
 @pytest.mark.parametrize("name", sorted(SMALL_GRAPHS))
 @pytest.mark.parametrize("spf", [1, 3])
 def test_frames_small(name, spf):
