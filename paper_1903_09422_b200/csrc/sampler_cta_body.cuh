@@ -15,18 +15,23 @@ constexpr uint32_t kSmallStep = 64;  // backtrack steps with deg(cur) <= this ru
 __device__ __forceinline__ bool m_is_t(uint32_t m) { return (m & kMetaT) != 0; }
 __device__ __forceinline__ uint32_t m_dist(uint32_t m) { return m & kMetaDist; }
 
-using BlockScan = cub::BlockScan<uint32_t, kBT>;
 
 struct Shared {
-    typename BlockScan::TempStorage scan_tmp;
+    uint32_t wtot[kBT / 32];          // block scan: per-warp totals
     uint32_t scan[kBT];               // inclusive degree scan of the current chunk
     uint32_t cbase[kBT];              // off(u) - exclusive(u): nbr index = cbase[owner] + e
     uint32_t cslot[kBT];              // store slot of the chunk's frontier vertex
     unsigned long long cval[kBT];     // per-vertex payload (sigma of u)
     unsigned long long item;
-    uint32_t degsum;                  // adjacency total of the level being claimed (< 2^32: u32 offsets)
+    unsigned long long tick[2];       // next work item, double-buffered by loop parity
+    uint32_t tflag[2];                // fused: the previous sample completed its epoch
+    unsigned long long done_old;      // thread 0 (fused): Done counter before the last sample's increment
+    uint32_t pending;                 // thread 0 (fused): done_old belongs to an unprocessed completion
+    uint32_t recorded, last_d;        // thread 0: increments recorded / last distance (fused audit)
+    uint32_t lvl_cnt[3];              // per BFS level (slot = level % 3): vertices claimed,
+    uint32_t lvl_deg[3];              //   their adjacency total (< 2^32: u32 offsets),
+    uint32_t lvl_ins[3];              //   hash reservations (shared-memory store)
     uint32_t s_cnt, t_cnt;            // queue fill: s-side from 0 up, t-side from the top down
-    uint32_t inserted;                // hash reservations this sample
     uint32_t overflow;
     uint32_t tlev_small[kSmemLevels]; // t-level boundaries (shared-memory store)
     unsigned long long wlo[kBT / 32]; // backtrack: per-warp 65-bit candidate sums
@@ -61,7 +66,13 @@ struct SmemStore {
     uint32_t limit;    // max insertions (<= capacity/2 keeps probing short and finite)
     uint32_t level_cap;
     Shared* sh;
+    uint32_t* ins_ctr;  // this level's reservation counter (Shared::lvl_ins slot)
+    uint32_t ins_base;  // reservations made before this level (same in every thread)
 
+    __device__ void set_level(uint32_t* ctr, uint32_t base) {
+        ins_ctr = ctr;
+        ins_base = base;
+    }
     __device__ uint32_t home(uint32_t v) const {
         return ((v * 0x9E3779B1u) >> shift) & mask;  // Fibonacci hashing on 32 bits
     }
@@ -119,6 +130,7 @@ struct SmemStore {
     // returns the slot (kNone on overflow); inserted tells whether this call created it
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
+        meta = ~0u;  // on overflow: matches no side/level test
         uint32_t h = home(v);
         bool reserved = false;
         for (;;) {
@@ -130,7 +142,7 @@ struct SmemStore {
             }
             if (k == kEmptyKey) {
                 if (!reserved) {
-                    if (atomicAdd(&sh->inserted, 1u) >= limit) {
+                    if (atomicAdd(ins_ctr, 1u) + ins_base >= limit) {
                         sh->overflow = 1;
                         return kNone;
                     }
@@ -177,8 +189,7 @@ struct SmemStore {
     // A one-pass (speculative) level is safe when it cannot claim more vertices
     // than the table has left: the level claims at most its adjacency count.
     __device__ bool room_for(unsigned long long edges) const {
-        const uint32_t used = sh->inserted;
-        return used < limit && edges <= limit - used;
+        return ins_base < limit && edges <= limit - ins_base;
     }
 };
 
@@ -230,6 +241,7 @@ struct GlobalStoreT {
     __device__ bool queue_ok(uint32_t, uint32_t) const { return true; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
     __device__ bool room_for(unsigned long long) const { return true; }
+    __device__ void set_level(uint32_t*, uint32_t) {}
 };
 
 struct Ctx {
@@ -240,11 +252,30 @@ struct Ctx {
     uint32_t warp;
     Shared* sh;
     unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
-    uint32_t recorded;  // increments recorded by this thread (thread 0 records)
-    uint32_t last_d;    // distance of the last sample (diagnostics)
     uint32_t n;
     bool low_degree;
 };
+
+// Inclusive prefix sum over the block (warp shuffles + per-warp totals, one
+// barrier). sh.wtot is rewritten only after the caller's next barrier.
+__device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint32_t& total) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, d);
+        if (C.lane >= static_cast<uint32_t>(d)) x += y;
+    }
+    if (C.lane == 31) C.sh->wtot[C.warp] = x;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < kBT / 32; ++w) {
+        const uint32_t t = C.sh->wtot[w];
+        pre += w < C.warp ? t : 0u;
+        tot += t;
+    }
+    total = tot;
+    return x + pre;
+}
 
 // Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
 // t_list). prep(slot) gives the per-vertex payload; body(slot_u, payload, v)
@@ -287,8 +318,8 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             slot = S.find(u, meta);
             val = prep(slot, meta, deg);
         }
-        uint32_t incl, total;
-        BlockScan(sh.scan_tmp).InclusiveSum(deg, incl, total);
+        uint32_t total;
+        const uint32_t incl = block_inclusive_sum(C, deg, total);
         sh.scan[C.tid] = incl;
         sh.cbase[C.tid] = o - (incl - deg);
         sh.cslot[C.tid] = slot;
@@ -347,9 +378,9 @@ __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int s
 }
 
 // One shared atomic per warp for the level's adjacency total.
-__device__ __forceinline__ void add_degsum(Ctx& C, uint32_t my_deg) {
+__device__ __forceinline__ void add_degsum(Ctx& C, uint32_t my_deg, uint32_t slot) {
     const uint32_t w = __reduce_add_sync(kFull, my_deg);
-    if (C.lane == 0 && w) atomicAdd(&C.sh->degsum, w);
+    if (C.lane == 0 && w) atomicAdd(&C.sh->lvl_deg[slot], w);
 }
 
 // Result of the BFS phase: distance split d = a + b + 1.
@@ -361,7 +392,13 @@ struct Meet {
 template <class Store>
 __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     Shared& sh = *C.sh;
+    // Level L = a + b uses counter slot L % 3; thread 0 zeroes slot (L+1) % 3
+    // as level L starts: every thread read that slot (as level L-2's) before
+    // level L-1's barriers, and level L+1 writes it only after level L's.
+    // So a level needs no barrier of its own before it starts claiming.
+    S.set_level(&sh.lvl_ins[2], 0);
     if (C.tid == 0) {
+        for (int i = 0; i < 3; ++i) sh.lvl_cnt[i] = sh.lvl_deg[i] = sh.lvl_ins[i] = 0;
         bool ins;
         uint32_t m;
         const uint32_t ss = S.claim(s, 0u, ins, m);
@@ -380,16 +417,17 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     }
     __syncthreads();
     uint32_t s_lo = 0, s_hi = 1, t_lo = 0, t_hi = 1, a = 0, b = 0;
+    uint32_t used = sh.lvl_ins[2];  // reservations so far (s and t)
     unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
     for (;;) {
+        const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
+        if (C.tid == 0) sh.lvl_cnt[nxt] = sh.lvl_deg[nxt] = sh.lvl_ins[nxt] = 0;
+        S.set_level(&sh.lvl_ins[cur], used);
         if (deg_s <= deg_t && S.room_for(deg_s)) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
             C.verts += C.tid == 0 ? s_hi - s_lo : 0;
             bool met = false;
-            __syncthreads();  // every thread has read the previous level's degsum
-            if (C.tid == 0) sh.degsum = 0;
-            __syncthreads();
             uint32_t my_deg = 0;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
@@ -400,9 +438,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (ins) {
                               S.zero_sigma(sl);
                               if (Store::kSigmaPreZeroed) S.add_sigma(sl, su);
-                              const uint32_t pos = atomicAdd(&sh.s_cnt, 1u);
+                              const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              ADSB_DCHECK(pos + sh.t_cnt <= S.qcap);
+                              ADSB_DCHECK(pos + t_hi < S.qcap);
                               S.qv[pos] = v;
                               S.qdeg[pos] = dg;
                               my_deg += dg;
@@ -414,8 +452,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                           }
                       });
-            add_degsum(C, my_deg);
-            if (__syncthreads_or(met)) return {a, b, 0};
+            add_degsum(C, my_deg, cur);
+            met = __syncthreads_or(met);
+            const uint32_t added = sh.lvl_cnt[cur];
+            if (met) {
+                if (C.tid == 0) sh.s_cnt = s_hi + added;  // the table clear walks the queue
+                return {a, b, 0};
+            }
             if (!Store::kSigmaPreZeroed)
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
@@ -424,19 +467,17 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.find(v, m);
                           if (sl != kNone && !m_is_t(m) && m_dist(m) == a + 1) S.add_sigma(sl, su);
                       });
-            __syncthreads();  // pre-zeroed stores skip the sigma pass: s_cnt/degsum final here
             s_lo = s_hi;
-            s_hi = sh.s_cnt;
-            deg_s = sh.degsum;
+            s_hi += added;
+            deg_s = sh.lvl_deg[cur];
+            used += sh.lvl_ins[cur];
             a += 1;
+            if (C.tid == 0) sh.s_cnt = s_hi;
             if (s_lo == s_hi) return {a, b, 2};
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             C.verts += C.tid == 0 ? t_hi - t_lo : 0;
             bool met = false;
-            __syncthreads();  // every thread has read the previous level's degsum
-            if (C.tid == 0) sh.degsum = 0;
-            __syncthreads();
             uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
@@ -447,9 +488,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.claim(v, meta_new, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t j = atomicAdd(&sh.t_cnt, 1u);
+                              const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              ADSB_DCHECK(j + sh.s_cnt <= S.qcap);
+                              ADSB_DCHECK(j + s_hi < S.qcap);
                               S.qv[S.tpos(j)] = v;
                               S.qdeg[S.tpos(j)] = dg;
                               my_deg += dg;
@@ -459,16 +500,23 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               met = true;
                           }
                       });
-            add_degsum(C, my_deg);
-            if (__syncthreads_or(met)) return {a, b, 0};
+            add_degsum(C, my_deg, cur);
+            met = __syncthreads_or(met);
+            const uint32_t added = sh.lvl_cnt[cur];
+            if (met) {
+                if (C.tid == 0) sh.t_cnt = t_hi + added;
+                return {a, b, 0};
+            }
             t_lo = t_hi;
-            t_hi = sh.t_cnt;
-            deg_t = sh.degsum;
+            t_hi += added;
+            deg_t = sh.lvl_deg[cur];
+            used += sh.lvl_ins[cur];
             b += 1;
+            if (C.tid == 0) {
+                sh.t_cnt = t_hi;
+                if (b + 2 <= S.level_cap) S.tlev[b + 1] = t_hi;  // read only after later barriers
+            }
             if (b + 2 > S.level_cap) return {a, b, 1};
-            ADSB_DCHECK(b + 1 < S.level_cap);
-            if (C.tid == 0) S.tlev[b + 1] = t_hi;
-            __syncthreads();
             if (t_lo == t_hi) return {a, b, 2};
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
@@ -487,8 +535,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             if (__syncthreads_or(met)) return {a, b, 0};
             // ---- no meeting: claim level a+1, then accumulate its sigma
-            if (C.tid == 0) sh.degsum = 0;
-            __syncthreads();
             uint32_t my_deg = 0;
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
@@ -501,9 +547,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t pos = atomicAdd(&sh.s_cnt, 1u);
+                              const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              if (S.queue_ok(pos + 1, sh.t_cnt)) {
+                              if (S.queue_ok(pos + 1, t_hi)) {
                                   S.qv[pos] = v;
                                   S.qdeg[pos] = dg;
                               } else {
@@ -512,8 +558,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               my_deg += dg;
                           }
                       });
-            add_degsum(C, my_deg);
-            __syncthreads();  // degsum complete before any thread reads it (uniform side choice)
+            add_degsum(C, my_deg, cur);
+            __syncthreads();  // counters and overflow final before any thread reads them
+            const uint32_t added = sh.lvl_cnt[cur];
+            if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
             if (!Store::kSigmaPreZeroed)
             for_edges(C, S, s_lo, s_hi, false, C.edges,
@@ -524,8 +572,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (sl != kNone && !m_is_t(m) && m_dist(m) == a + 1) S.add_sigma(sl, su);
                       });
             s_lo = s_hi;
-            s_hi = sh.s_cnt;
-            deg_s = sh.degsum;
+            s_hi += added;
+            deg_s = sh.lvl_deg[cur];
+            used += sh.lvl_ins[cur];
             a += 1;
             if (s_lo == s_hi) return {a, b, 2};
         } else {
@@ -544,8 +593,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           }
                       });
             if (__syncthreads_or(met)) return {a, b, 0};
-            if (C.tid == 0) sh.degsum = 0;
-            __syncthreads();
             uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
@@ -556,9 +603,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.claim(v, meta_new, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t j = atomicAdd(&sh.t_cnt, 1u);
+                              const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
                               const uint32_t dg = C.off[v + 1] - C.off[v];
-                              if (S.queue_ok(sh.s_cnt, j + 1)) {
+                              if (S.queue_ok(s_hi, j + 1)) {
                                   S.qv[S.tpos(j)] = v;
                                   S.qdeg[S.tpos(j)] = dg;
                               } else {
@@ -567,17 +614,18 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               my_deg += dg;
                           }
                       });
-            add_degsum(C, my_deg);
+            add_degsum(C, my_deg, cur);
             __syncthreads();
+            const uint32_t added = sh.lvl_cnt[cur];
+            if (C.tid == 0) sh.t_cnt = min(t_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
             t_lo = t_hi;
-            t_hi = sh.t_cnt;
-            deg_t = sh.degsum;
+            t_hi += added;
+            deg_t = sh.lvl_deg[cur];
+            used += sh.lvl_ins[cur];
             b += 1;
+            if (C.tid == 0 && b + 2 <= S.level_cap) S.tlev[b + 1] = t_hi;
             if (b + 2 > S.level_cap) return {a, b, 1};
-            ADSB_DCHECK(b + 1 < S.level_cap);
-            if (C.tid == 0) S.tlev[b + 1] = t_hi;
-            __syncthreads();
             if (t_lo == t_hi) return {a, b, 2};
         }
     }
@@ -633,7 +681,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
     Shared& sh = *C.sh;
     constexpr uint32_t kNW = kBT / 32;
     const uint32_t d = mt.a + mt.b + 1;
-    C.last_d = d;
+    if (C.tid == 0) sh.last_d = d;
     if (d < 2) return true;
     constexpr bool kDet = kMode == kModeDet;
     if (kDet && C.tid == 0) sh.ev_pos = atomicAdd(p.ev_cursor, static_cast<unsigned long long>(d - 1));
@@ -818,7 +866,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                 atomicAdd(p.counts + cur, 1u);
             } else {
                 // fused: frame_local is the ring slot; record first touches for the fold
-                ++C.recorded;
+                ++sh.recorded;
                 const size_t base = static_cast<size_t>(frame_local) * p.n;
                 if (atomicAdd(p.ring_cnt + base + cur, 1u) == 0u)
                     p.ring_list[base + atomicAdd(p.ring_len + frame_local, 1u)] = cur;
@@ -837,7 +885,6 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
     Shared& sh = *C.sh;
     S.begin(C.tid);
     if (C.tid == 0) {
-        sh.inserted = 0;
         sh.overflow = 0;
     }
     __syncthreads();
@@ -867,7 +914,7 @@ __device__ void one_sample(Ctx& C, SmemStore& sm, GS& gs, const SamplerParams& p
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
     uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
     if (t >= s) ++t;
-    C.last_d = 0xFFFF;
+    if (C.tid == 0) C.sh->last_d = 0xFFFF;
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
     int rc = 1;
     if constexpr (!kGlobalOnly) {
@@ -985,8 +1032,6 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
     C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
-    C.recorded = 0;
-    C.last_d = 0;
     C.n = p.n;
     C.low_degree = p.max_degree <= 32;
     const uint32_t slot = blockIdx.x;
@@ -1017,12 +1062,22 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     if constexpr (!kGlobalOnly) sm.clear_all(C.tid);
     __syncthreads();
     unsigned long long samples = 0, fallbacks = 0, errors = 0;
+    // The published ticket is double-buffered by loop parity: one barrier per
+    // sample (slot `par` is rewritten two iterations later, after every thread
+    // passed the next barrier). Tickets are not fetched ahead: a block holding
+    // a second ticket through a long sample delays the tail (measured on C4).
+    if (C.tid == 0) {
+        sh.recorded = 0;
+        sh.last_d = 0;
+        sh.pending = 0;
+        sh.done_old = 0;
+    }
     if (kMode != kModeFused) {
-        for (;;) {
-            if (C.tid == 0) sh.item = atomicAdd(p.ticket, 1ull);
+        for (uint32_t it = 0;; ++it) {
+            const uint32_t par = it & 1;
+            if (C.tid == 0) sh.tick[par] = atomicAdd(p.ticket, 1ull);
             __syncthreads();
-            const unsigned long long item = sh.item;
-            __syncthreads();
+            const unsigned long long item = sh.tick[par];
             if (item >= p.num_items) break;
             const uint64_t local = item * p.world + p.rank;
             SplitMix64 rng(reseed(p.seed, p.first + local));
@@ -1036,39 +1091,49 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
         // start epoch e only once epoch e - K has been folded (its slot is free);
         // every earlier epoch's samples are already held by running blocks, so
         // the wait always ends (one persistent grid, all blocks resident).
-        for (;;) {
+        // A sample's completion (Done counter) is issued after it and read at
+        // the top of the next iteration: a block that completed an epoch folds
+        // it before it may wait on a ring slot (its ticket is taken afterwards).
+        for (uint32_t it = 0;; ++it) {
+            const uint32_t par = it & 1;
             if (C.tid == 0) {
-                unsigned long long i = atomicAdd(p.ctl + kCtlTicket, 1ull);
-                const unsigned long long e = i / p.epoch_b;
-                for (;;) {
-                    if (e > vload(p.ctl + kCtlStop) || e >= p.max_epochs) {
-                        i = ~0ull;
-                        break;
+                const bool completed = sh.pending && sh.done_old + 1 == p.epoch_b;
+                sh.pending = 0;
+                unsigned long long i = ~0ull;
+                if (!completed) {
+                    i = atomicAdd(p.ctl + kCtlTicket, 1ull);
+                    const unsigned long long e = i / p.epoch_b;
+                    for (;;) {
+                        if (e > vload(p.ctl + kCtlStop) || e >= p.max_epochs) {
+                            i = ~0ull;
+                            break;
+                        }
+                        if (e < vload(p.ctl + kCtlFolded) + p.ring_k) break;
+                        __nanosleep(200);
                     }
-                    if (e < vload(p.ctl + kCtlFolded) + p.ring_k) break;
-                    __nanosleep(200);
                 }
-                sh.item = i;
+                sh.tick[par] = i;
+                sh.tflag[par] = completed ? 1u : 0u;
             }
             __syncthreads();
-            const unsigned long long item = sh.item;
-            __syncthreads();
+            const unsigned long long item = sh.tick[par];
+            if (sh.tflag[par]) {
+                fold_chain(C, p);
+                continue;
+            }
             if (item == ~0ull) break;
             const uint32_t k = static_cast<uint32_t>((item / p.epoch_b) % p.ring_k);
             SplitMix64 rng(reseed(p.seed, item));
             ++samples;
-            const uint32_t rec0 = C.recorded;
+            const uint32_t rec0 = sh.recorded;
             one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, k, fallbacks, errors);
             if (C.tid == 0) {
                 if (p.audit && item < p.max_epochs * p.epoch_b)
-                    p.audit[item] = (C.recorded - rec0) | (C.last_d << 16);
+                    p.audit[item] = (sh.recorded - rec0) | (sh.last_d << 16);
                 __threadfence();  // this sample's counts before its completion
-                sh.flag = atomicAdd(p.ctl + kCtlDone + k, 1ull) + 1 == p.epoch_b ? 1u : 0u;
+                sh.done_old = atomicAdd(p.ctl + kCtlDone + k, 1ull);
+                sh.pending = 1;
             }
-            __syncthreads();
-            const bool completed = sh.flag != 0;
-            __syncthreads();
-            if (completed) fold_chain(C, p);
         }
     }
     // per-thread counters: reduce across the block once
