@@ -58,7 +58,6 @@ struct SmemStore {
     unsigned long long* km;
     unsigned long long* sig;
     uint32_t* qv;      // queue: vertex ids
-    uint32_t* qdeg;    // queue: degrees (for the side-balancing heuristic)
     uint32_t* tlev;
     uint32_t mask;
     uint32_t shift;
@@ -201,7 +200,6 @@ struct GlobalStoreT {
     static constexpr uint32_t kUnrollEdges = kU;
     unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
     uint32_t* qv;
-    uint32_t* qdeg;
     uint32_t* tlev;
     uint32_t tag;
     uint32_t qcap;
@@ -383,6 +381,33 @@ __device__ __forceinline__ void add_degsum(Ctx& C, uint32_t my_deg, uint32_t slo
     if (C.lane == 0 && w) atomicAdd(&C.sh->lvl_deg[slot], w);
 }
 
+// Adjacency total of queue entries [lo, hi) (a newly claimed level), for the
+// side-balancing choice. One parallel pass after the level's barrier: the
+// offset loads overlap (4 in flight per thread) instead of stalling each claim.
+template <class Store>
+__device__ uint32_t level_degrees(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, uint32_t slot) {
+    uint32_t my = 0;
+    for (uint32_t i0 = lo + C.tid; i0 < hi; i0 += 4 * kBT) {
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = i0 + k * kBT;
+            v[k] = i < hi ? S.qv[t_list ? S.tpos(i) : i] : kNone;
+        }
+        uint32_t lo_off[4], hi_off[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            lo_off[k] = v[k] != kNone ? C.off[v[k]] : 0u;
+            hi_off[k] = v[k] != kNone ? C.off[v[k] + 1] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) my += hi_off[k] - lo_off[k];
+    }
+    add_degsum(C, my, slot);
+    __syncthreads();
+    return C.sh->lvl_deg[slot];
+}
+
 // Result of the BFS phase: distance split d = a + b + 1.
 struct Meet {
     uint32_t a, b;
@@ -407,9 +432,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         S.zero_sigma(tt);
         S.add_sigma(ss, 1ull);
         S.qv[0] = s;
-        S.qdeg[0] = C.off[s + 1] - C.off[s];
         S.qv[S.tpos(0)] = t;
-        S.qdeg[S.tpos(0)] = C.off[t + 1] - C.off[t];
         S.tlev[0] = 0;
         S.tlev[1] = 1;
         sh.s_cnt = 1;
@@ -428,7 +451,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // Claims made on the meeting level are harmless (never predecessors).
             C.verts += C.tid == 0 ? s_hi - s_lo : 0;
             bool met = false;
-            uint32_t my_deg = 0;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -439,11 +461,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.zero_sigma(sl);
                               if (Store::kSigmaPreZeroed) S.add_sigma(sl, su);
                               const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
-                              const uint32_t dg = C.off[v + 1] - C.off[v];
                               ADSB_DCHECK(pos + t_hi < S.qcap);
                               S.qv[pos] = v;
-                              S.qdeg[pos] = dg;
-                              my_deg += dg;
                           } else if (m_is_t(m) && m_dist(m) == b) {
                               S.add_sigma(sl, su);
                               if (!(m & kMetaDag)) S.set_dag(sl);
@@ -452,7 +471,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                           }
                       });
-            add_degsum(C, my_deg, cur);
             met = __syncthreads_or(met);
             const uint32_t added = sh.lvl_cnt[cur];
             if (met) {
@@ -469,16 +487,15 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             s_lo = s_hi;
             s_hi += added;
-            deg_s = sh.lvl_deg[cur];
             used += sh.lvl_ins[cur];
             a += 1;
             if (C.tid == 0) sh.s_cnt = s_hi;
             if (s_lo == s_hi) return {a, b, 2};
+            deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             C.verts += C.tid == 0 ? t_hi - t_lo : 0;
             bool met = false;
-            uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -489,18 +506,14 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (ins) {
                               S.zero_sigma(sl);
                               const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
-                              const uint32_t dg = C.off[v + 1] - C.off[v];
                               ADSB_DCHECK(j + s_hi < S.qcap);
                               S.qv[S.tpos(j)] = v;
-                              S.qdeg[S.tpos(j)] = dg;
-                              my_deg += dg;
                           } else if (!m_is_t(m) && m_dist(m) == a) {
                               S.add_sigma(su_slot, S.sigma(sl));
                               S.set_dag(su_slot);
                               met = true;
                           }
                       });
-            add_degsum(C, my_deg, cur);
             met = __syncthreads_or(met);
             const uint32_t added = sh.lvl_cnt[cur];
             if (met) {
@@ -509,7 +522,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             }
             t_lo = t_hi;
             t_hi += added;
-            deg_t = sh.lvl_deg[cur];
             used += sh.lvl_ins[cur];
             b += 1;
             if (C.tid == 0) {
@@ -518,6 +530,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             }
             if (b + 2 > S.level_cap) return {a, b, 1};
             if (t_lo == t_hi) return {a, b, 2};
+            deg_t = level_degrees(C, S, t_lo, t_hi, true, cur);
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
             C.verts += C.tid == 0 ? s_hi - s_lo : 0;
@@ -535,7 +548,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             if (__syncthreads_or(met)) return {a, b, 0};
             // ---- no meeting: claim level a+1, then accumulate its sigma
-            uint32_t my_deg = 0;
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, C.edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return Store::kSigmaPreZeroed ? S.sigma(slot) : 0ull; },
@@ -548,17 +560,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (ins) {
                               S.zero_sigma(sl);
                               const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
-                              const uint32_t dg = C.off[v + 1] - C.off[v];
-                              if (S.queue_ok(pos + 1, t_hi)) {
-                                  S.qv[pos] = v;
-                                  S.qdeg[pos] = dg;
-                              } else {
-                                  sh.overflow = 1;
-                              }
-                              my_deg += dg;
+                              if (S.queue_ok(pos + 1, t_hi)) S.qv[pos] = v;
+                              else sh.overflow = 1;
                           }
                       });
-            add_degsum(C, my_deg, cur);
             __syncthreads();  // counters and overflow final before any thread reads them
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
@@ -573,10 +578,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             s_lo = s_hi;
             s_hi += added;
-            deg_s = sh.lvl_deg[cur];
             used += sh.lvl_ins[cur];
             a += 1;
             if (s_lo == s_hi) return {a, b, 2};
+            deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
         } else {
             // ---- t-side level b: probe for the s-ball
             C.verts += C.tid == 0 ? t_hi - t_lo : 0;
@@ -593,7 +598,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           }
                       });
             if (__syncthreads_or(met)) return {a, b, 0};
-            uint32_t my_deg = 0;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, C.edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -604,29 +608,22 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (ins) {
                               S.zero_sigma(sl);
                               const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
-                              const uint32_t dg = C.off[v + 1] - C.off[v];
-                              if (S.queue_ok(s_hi, j + 1)) {
-                                  S.qv[S.tpos(j)] = v;
-                                  S.qdeg[S.tpos(j)] = dg;
-                              } else {
-                                  sh.overflow = 1;
-                              }
-                              my_deg += dg;
+                              if (S.queue_ok(s_hi, j + 1)) S.qv[S.tpos(j)] = v;
+                              else sh.overflow = 1;
                           }
                       });
-            add_degsum(C, my_deg, cur);
             __syncthreads();
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.t_cnt = min(t_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
             t_lo = t_hi;
             t_hi += added;
-            deg_t = sh.lvl_deg[cur];
             used += sh.lvl_ins[cur];
             b += 1;
             if (C.tid == 0 && b + 2 <= S.level_cap) S.tlev[b + 1] = t_hi;
             if (b + 2 > S.level_cap) return {a, b, 1};
             if (t_lo == t_hi) return {a, b, 2};
+            deg_t = level_degrees(C, S, t_lo, t_hi, true, cur);
         }
     }
 }
@@ -1042,7 +1039,6 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     sm.sig = dyn + H;
     sm.qcap = H / 2;
     sm.qv = reinterpret_cast<uint32_t*>(dyn + 2 * H);
-    sm.qdeg = sm.qv + sm.qcap;
     sm.tlev = sh.tlev_small;
     sm.mask = H - 1;
     sm.shift = 32 - (31 - __clz(H));
@@ -1053,7 +1049,6 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     GlobalStoreT<1> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
-    gs.qdeg = reinterpret_cast<uint32_t*>(p.qrange + static_cast<size_t>(p.slot_stride) * slot);
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
     gs.tag = p.slot_tag[slot];
     gs.qcap = p.n;
