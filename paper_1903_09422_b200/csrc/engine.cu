@@ -855,6 +855,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             out.reason = ADSB_REASON_EPS_CONVERGED;
     }
     out.ads_seconds = ads.seconds();
+    if (trace_enabled()) sampler_phase_report();
     return out;
 }
 

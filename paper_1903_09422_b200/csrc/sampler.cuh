@@ -101,6 +101,8 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
 int sampler_global_blocks_per_sm();
 // single-launch epoch pipeline with device-side folding and stopping (block teams)
 void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream);
+// diagnostic builds (-DADSB_PHASE_TIMING): print and reset per-phase cycle sums
+void sampler_phase_report();
 
 enum class SamplerKind { kWarp, kBlock };
 SamplerKind sampler_kind();  // ADSB_SAMPLER=warp|block (default block)

@@ -25,19 +25,40 @@
 //
 // The sigma-weighted backtrack (kadabra.hpp:227-242) is block-wide: a 65-bit
 // block prefix sum over the ascending-neighbour candidates per round.
-#include <cub/block/block_scan.cuh>
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "device.cuh"
 #include "rng.hpp"
 #include "sampler.cuh"
 
-#ifndef ADSB_UNROLL
-#define ADSB_UNROLL 1  // adjacency loads in flight per thread in for_edges
+#ifndef ADSB_LOAD_BATCH
+#define ADSB_LOAD_BATCH 1  // adjacency loads in flight per thread in for_edges (A/B: 1 beats 2 and 4)
 #endif
 #ifndef ADSB_MINB_PER_256
 #define ADSB_MINB_PER_256 4  // __launch_bounds__ min blocks for 256-thread blocks (register budget)
+#endif
+
+// ADSB_PHASE_TIMING (diagnostic builds only): thread 0 of every block adds
+// clock64 deltas per sampler phase into adsb_phase[]; sampler_phase_report()
+// prints and resets them.
+#ifdef ADSB_PHASE_TIMING
+__device__ unsigned long long adsb_phase[8];
+#define ADSB_PHASE_MARK(x) const long long x = clock64()
+#define ADSB_PHASE_ADD(i, v) \
+    do {                     \
+        if (threadIdx.x == 0) atomicAdd(&adsb_phase[i], static_cast<unsigned long long>(v)); \
+    } while (0)
+#else
+#define ADSB_PHASE_MARK(x) \
+    do {                   \
+    } while (0)
+#define ADSB_PHASE_ADD(i, v) \
+    do {                     \
+    } while (0)
 #endif
 
 #ifdef ADSB_DEBUG_CHECKS
@@ -146,6 +167,21 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused, false><<<p.slots, 128, dyn, stream>>>(p);
     else bt256::sampler_cta_kernel<kModeFused, false><<<p.slots, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
+}
+
+void sampler_phase_report() {
+#ifdef ADSB_PHASE_TIMING
+    unsigned long long h[8];
+    cudaMemcpyFromSymbol(h, adsb_phase, sizeof(h));
+    const double samples = h[7] ? static_cast<double>(h[7]) : 1.0;
+    std::fprintf(stderr,
+                 "[adsb] phase cycles per sample (thread 0): bfs %.0f rebuild %.0f backtrack %.0f clear %.0f | "
+                 "kernel per block %.3g, samples %llu, levels/sample %.2f, edge passes/sample %.2f\n",
+                 h[0] / samples, h[1] / samples, h[2] / samples, h[3] / samples, static_cast<double>(h[4]),
+                 h[7], h[5] / samples, h[6] / samples);
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(adsb_phase, z, sizeof(z));
+#endif
 }
 
 }  // namespace adsb

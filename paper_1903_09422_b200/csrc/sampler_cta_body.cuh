@@ -18,6 +18,7 @@ __device__ __forceinline__ uint32_t m_dist(uint32_t m) { return m & kMetaDist; }
 
 struct Shared {
     uint32_t wtot[kBT / 32];          // block scan: per-warp totals
+    uint32_t stage[4][kBT];           // for_edges: each thread's batch of adjacency ids
     uint32_t scan[kBT];               // inclusive degree scan of the current chunk
     uint32_t cbase[kBT];              // off(u) - exclusive(u): nbr index = cbase[owner] + e
     uint32_t cslot[kBT];              // store slot of the chunk's frontier vertex
@@ -54,7 +55,7 @@ struct Shared {
 // Empty slots have key 0xFFFFFFFF and sigma 0 (sigma is zeroed with the key,
 // so concurrent claimers and adders never race on initialisation).
 struct SmemStore {
-    static constexpr uint32_t kUnrollEdges = ADSB_UNROLL;
+    static constexpr uint32_t kLoadBatch = ADSB_LOAD_BATCH;
     unsigned long long* km;
     unsigned long long* sig;
     uint32_t* qv;      // queue: vertex ids
@@ -126,12 +127,15 @@ struct SmemStore {
             h = (h + 1) & mask;
         }
     }
-    // returns the slot (kNone on overflow); inserted tells whether this call created it
+    // returns the slot (kNone on overflow); inserted tells whether this call
+    // created it. kReserve = false: the caller guarantees capacity (room_for),
+    // so no reservation counter is touched.
+    template <bool kReserve = true>
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
         meta = ~0u;  // on overflow: matches no side/level test
         uint32_t h = home(v);
-        bool reserved = false;
+        bool reserved = !kReserve;
         for (;;) {
             unsigned long long x = km[h];
             uint32_t k = static_cast<uint32_t>(x >> 32);
@@ -197,7 +201,7 @@ struct SmemStore {
 // kernel trades registers for memory-level parallelism).
 template <uint32_t kU>
 struct GlobalStoreT {
-    static constexpr uint32_t kUnrollEdges = kU;
+    static constexpr uint32_t kLoadBatch = kU;
     unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* tlev;
@@ -214,6 +218,7 @@ struct GlobalStoreT {
         meta = static_cast<uint32_t>(x);
         return v;
     }
+    template <bool kReserve = true>
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
         unsigned long long x = __ldcg(st + 2ull * v);
@@ -282,6 +287,7 @@ template <class Store, class Prep, class Body>
 __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long& counter,
                           Prep prep, Body body) {
     Shared& sh = *C.sh;
+    ADSB_PHASE_ADD(6, 1);
     if (C.low_degree) {
         // Low-degree graphs (max degree <= 32, e.g. the grid): one thread per
         // frontier vertex walks its whole adjacency; no scan, no chunk
@@ -296,7 +302,14 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             const uint32_t slot = S.find(u, meta);
             const unsigned long long val = prep(slot, meta, e - o);
             mine += e - o;
-            for (uint32_t j = o; j < e; ++j) body(slot, val, C.nbrs[j]);
+            for (uint32_t j0 = o; j0 < e; j0 += 4) {
+                uint32_t vv[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.nbrs[j0 + k] : kNone;
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    if (vv[k] != kNone) body(slot, val, vv[k]);
+            }
         }
         counter += mine;
         __syncthreads();
@@ -330,18 +343,20 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         // remaining populated entries only) when e passes that owner's end:
         // O(1) per edge inside hub adjacency lists.
         const uint32_t populated = min(hi - base, static_cast<uint32_t>(kBT));
-        uint32_t ow = 0, o_end = 0, o_base = 0, o_slot = 0;
-        unsigned long long o_val = 0;
+        uint32_t ow = 0, o_end = 0, o_base = 0;
         bool have = false;
-        // kUnroll adjacency loads in flight per thread before any is consumed
-        constexpr uint32_t kUnroll = Store::kUnrollEdges;
-        for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kUnroll) {
-            uint32_t vv[kUnroll], vs[kUnroll];
-            unsigned long long vval[kUnroll];
+        // kBatch adjacency loads in flight per thread before any body runs.
+        // The ids are staged in shared memory (a register array indexed by a
+        // runtime k would spill) and one non-unrolled loop runs the body, so
+        // the body is instantiated once (unrolled copies overflow the
+        // instruction cache). Owner indices pack into one register (8 bits).
+        constexpr uint32_t kBatch = Store::kLoadBatch;
+        static_assert(kBT <= 256 && kBatch <= 4, "owner indices pack into 32 bits");
+        for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kBatch) {
+            uint32_t owners = 0, cnt = 0;
 #pragma unroll
-            for (uint32_t k = 0; k < kUnroll; ++k) {
+            for (uint32_t k = 0; k < kBatch; ++k) {
                 const uint32_t e = e0 + k * kBT;
-                vv[k] = kNone;
                 if (e < total) {
                     if (!have || e >= o_end) {
                         uint32_t l = have ? ow + 1 : 0, r = populated - 1;
@@ -353,19 +368,20 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                         ow = l;
                         o_end = sh.scan[ow];
                         o_base = sh.cbase[ow];
-                        o_slot = sh.cslot[ow];
-                        o_val = sh.cval[ow];
                         have = true;
                     }
-                    vv[k] = C.nbrs[o_base + e];
-                    ADSB_DCHECK(vv[k] < C.n);
-                    vs[k] = o_slot;
-                    vval[k] = o_val;
+                    sh.stage[k][C.tid] = C.nbrs[o_base + e];
+                    owners |= ow << (8 * k);
+                    cnt = k + 1;
                 }
             }
-#pragma unroll
-            for (uint32_t k = 0; k < kUnroll; ++k)
-                if (vv[k] != kNone) body(vs[k], vval[k], vv[k]);
+#pragma unroll 1
+            for (uint32_t k = 0; k < cnt; ++k) {
+                const uint32_t v = sh.stage[k][C.tid];
+                ADSB_DCHECK(v < C.n);
+                const uint32_t w = (owners >> (8 * k)) & 0xFFu;
+                body(sh.cslot[w], sh.cval[w], v);
+            }
         }
         __syncthreads();
     }
@@ -373,6 +389,17 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int src) {
     return __shfl_sync(kFull, x, src);
+}
+
+// Next positions of a per-level counter for the converged lanes of a warp:
+// one shared atomic per group instead of one per lane (the counter is the
+// same address for the whole block).
+__device__ __forceinline__ uint32_t aggregated_inc(uint32_t* ctr) {
+    namespace cg = cooperative_groups;
+    const cg::coalesced_group g = cg::coalesced_threads();
+    uint32_t base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(ctr, g.size());
+    return g.shfl(base, 0) + g.thread_rank();
 }
 
 // One shared atomic per warp for the level's adjacency total.
@@ -456,11 +483,11 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           bool ins;
                           uint32_t m;
-                          const uint32_t sl = S.claim(v, a + 1, ins, m);
+                          const uint32_t sl = S.template claim<false>(v, a + 1, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
                               if (Store::kSigmaPreZeroed) S.add_sigma(sl, su);
-                              const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
+                              const uint32_t pos = s_hi + aggregated_inc(&sh.lvl_cnt[cur]);
                               ADSB_DCHECK(pos + t_hi < S.qcap);
                               S.qv[pos] = v;
                           } else if (m_is_t(m) && m_dist(m) == b) {
@@ -487,7 +514,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             s_lo = s_hi;
             s_hi += added;
-            used += sh.lvl_ins[cur];
+            used += added;  // one-pass claims reserve nothing: occupancy grew by the inserts
             a += 1;
             if (C.tid == 0) sh.s_cnt = s_hi;
             if (s_lo == s_hi) return {a, b, 2};
@@ -502,10 +529,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
                           bool ins;
                           uint32_t m;
-                          const uint32_t sl = S.claim(v, meta_new, ins, m);
+                          const uint32_t sl = S.template claim<false>(v, meta_new, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
+                              const uint32_t j = t_hi + aggregated_inc(&sh.lvl_cnt[cur]);
                               ADSB_DCHECK(j + s_hi < S.qcap);
                               S.qv[S.tpos(j)] = v;
                           } else if (!m_is_t(m) && m_dist(m) == a) {
@@ -522,7 +549,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             }
             t_lo = t_hi;
             t_hi += added;
-            used += sh.lvl_ins[cur];
+            used += added;  // one-pass claims reserve nothing: occupancy grew by the inserts
             b += 1;
             if (C.tid == 0) {
                 sh.t_cnt = t_hi;
@@ -559,7 +586,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t pos = s_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
+                              const uint32_t pos = s_hi + aggregated_inc(&sh.lvl_cnt[cur]);
                               if (S.queue_ok(pos + 1, t_hi)) S.qv[pos] = v;
                               else sh.overflow = 1;
                           }
@@ -607,7 +634,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           const uint32_t sl = S.claim(v, meta_new, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
-                              const uint32_t j = t_hi + atomicAdd(&sh.lvl_cnt[cur], 1u);
+                              const uint32_t j = t_hi + aggregated_inc(&sh.lvl_cnt[cur]);
                               if (S.queue_ok(s_hi, j + 1)) S.qv[S.tpos(j)] = v;
                               else sh.overflow = 1;
                           }
@@ -885,7 +912,11 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         sh.overflow = 0;
     }
     __syncthreads();
+    ADSB_PHASE_MARK(t0);
     const Meet mt = bfs(C, S, s, t);
+    ADSB_PHASE_MARK(t1);
+    ADSB_PHASE_ADD(0, t1 - t0);
+    ADSB_PHASE_ADD(5, mt.a + mt.b + 1);
 #ifdef ADSB_DEBUG_CHECKS
     if (mt.status == 0 && mt.a + mt.b == 0 && C.tid == 0) {
         bool adj = false;
@@ -898,8 +929,15 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         return mt.status;
     }
     rebuild(C, S, mt.b);
+    ADSB_PHASE_MARK(t2);
     const int rc = backtrack<kMode>(C, S, p, rng, t, mt, frame_local) ? 0 : 2;  // block-uniform
+    ADSB_PHASE_MARK(t3);
     S.end(C, sh);
+    ADSB_PHASE_MARK(t4);
+    ADSB_PHASE_ADD(1, t2 - t1);
+    ADSB_PHASE_ADD(2, t3 - t2);
+    ADSB_PHASE_ADD(3, t4 - t3);
+    ADSB_PHASE_ADD(7, 1);
     return rc;
 }
 
@@ -1046,7 +1084,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     sm.level_cap = kSmemLevels;
     sm.sh = &sh;
 
-    GlobalStoreT<1> gs;
+    GlobalStoreT<ADSB_LOAD_BATCH> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
@@ -1056,6 +1094,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
 
     if constexpr (!kGlobalOnly) sm.clear_all(C.tid);
     __syncthreads();
+    ADSB_PHASE_MARK(k0);
     unsigned long long samples = 0, fallbacks = 0, errors = 0;
     // The published ticket is double-buffered by loop parity: one barrier per
     // sample (slot `par` is rewritten two iterations later, after every thread
@@ -1131,6 +1170,8 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
             }
         }
     }
+    ADSB_PHASE_MARK(k1);
+    ADSB_PHASE_ADD(4, k1 - k0);
     // per-thread counters: reduce across the block once
     atomicAdd(p.stats + kStatEdges, C.edges + C.rebuild_edges + C.back_edges);
     atomicAdd(p.stats + kStatRebuildEdges, C.rebuild_edges);
