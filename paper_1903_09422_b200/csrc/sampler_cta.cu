@@ -46,7 +46,7 @@
 // clock64 deltas per sampler phase into adsb_phase[]; sampler_phase_report()
 // prints and resets them.
 #ifdef ADSB_PHASE_TIMING
-__device__ unsigned long long adsb_phase[8];
+__device__ unsigned long long adsb_phase[16];
 #define ADSB_PHASE_MARK(x) const long long x = clock64()
 #define ADSB_PHASE_ADD(i, v) \
     do {                     \
@@ -171,7 +171,7 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
 
 void sampler_phase_report() {
 #ifdef ADSB_PHASE_TIMING
-    unsigned long long h[8];
+    unsigned long long h[16];
     cudaMemcpyFromSymbol(h, adsb_phase, sizeof(h));
     const double samples = h[7] ? static_cast<double>(h[7]) : 1.0;
     std::fprintf(stderr,
@@ -179,7 +179,13 @@ void sampler_phase_report() {
                  "kernel per block %.3g, samples %llu, levels/sample %.2f, edge passes/sample %.2f\n",
                  h[0] / samples, h[1] / samples, h[2] / samples, h[3] / samples, static_cast<double>(h[4]),
                  h[7], h[5] / samples, h[6] / samples);
-    unsigned long long z[8] = {};
+    std::fprintf(stderr,
+                 "[adsb]   for_edges per chunk: prep %.0f, edge loop (thread 0) %.0f, end barrier wait %.0f | "
+                 "edges/chunk %.1f, chunks/sample %.2f, level degree passes %.0f per sample\n",
+                 h[13] ? h[8] / static_cast<double>(h[13]) : 0.0, h[13] ? h[9] / static_cast<double>(h[13]) : 0.0,
+                 h[13] ? h[11] / static_cast<double>(h[13]) : 0.0, h[13] ? h[12] / static_cast<double>(h[13]) : 0.0,
+                 h[13] / samples, h[10] / samples);
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(adsb_phase, z, sizeof(z));
 #endif
 }

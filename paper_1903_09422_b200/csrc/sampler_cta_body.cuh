@@ -18,7 +18,6 @@ __device__ __forceinline__ uint32_t m_dist(uint32_t m) { return m & kMetaDist; }
 
 struct Shared {
     uint32_t wtot[kBT / 32];          // block scan: per-warp totals
-    uint32_t stage[4][kBT];           // for_edges: each thread's batch of adjacency ids
     uint32_t scan[kBT];               // inclusive degree scan of the current chunk
     uint32_t cbase[kBT];              // off(u) - exclusive(u): nbr index = cbase[owner] + e
     uint32_t cslot[kBT];              // store slot of the chunk's frontier vertex
@@ -27,6 +26,8 @@ struct Shared {
     unsigned long long tick[2];       // next work item, double-buffered by loop parity
     uint32_t tflag[2];                // fused: the previous sample completed its epoch
     unsigned long long done_old;      // thread 0 (fused): Done counter before the last sample's increment
+    unsigned long long st_edges, st_rebuild, st_back, st_verts, st_degen;  // block statistics (thread 0 adds)
+    unsigned long long n_samples, n_fallbacks, n_errors;
     uint32_t pending;                 // thread 0 (fused): done_old belongs to an unprocessed completion
     uint32_t recorded, last_d;        // thread 0: increments recorded / last distance (fused audit)
     uint32_t lvl_cnt[3];              // per BFS level (slot = level % 3): vertices claimed,
@@ -254,7 +255,6 @@ struct Ctx {
     uint32_t lane;
     uint32_t warp;
     Shared* sh;
-    unsigned long long edges, rebuild_edges, back_edges, verts, degenerate;
     uint32_t n;
     bool low_degree;
 };
@@ -284,7 +284,7 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 // t_list). prep(slot) gives the per-vertex payload; body(slot_u, payload, v)
 // runs once per adjacency entry. Ends with a block barrier.
 template <class Store, class Prep, class Body>
-__device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long& counter,
+__device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long* counter,
                           Prep prep, Body body) {
     Shared& sh = *C.sh;
     ADSB_PHASE_ADD(6, 1);
@@ -311,11 +311,13 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                     if (vv[k] != kNone) body(slot, val, vv[k]);
             }
         }
-        counter += mine;
+        const uint32_t wm = __reduce_add_sync(kFull, static_cast<uint32_t>(mine));
+        if (C.lane == 0 && wm) atomicAdd(counter, static_cast<unsigned long long>(wm));
         __syncthreads();
         return;
     }
     for (uint32_t base = lo; base < hi; base += kBT) {
+        ADSB_PHASE_MARK(f0);
         const uint32_t i = base + C.tid;
         uint32_t deg = 0, o = 0, slot = 0;
         unsigned long long val = 0;
@@ -336,7 +338,11 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         sh.cslot[C.tid] = slot;
         sh.cval[C.tid] = val;
         __syncthreads();
-        counter += C.tid == 0 ? total : 0;
+        ADSB_PHASE_MARK(f1);
+        ADSB_PHASE_ADD(8, f1 - f0);
+        ADSB_PHASE_ADD(12, total);
+        ADSB_PHASE_ADD(13, 1);
+        if (C.tid == 0) *counter += total;
         // Owner of edge e = first chunk entry k with scan[k] > e. A thread's
         // edges e, e+kBT, ... have non-decreasing owners, so it keeps the
         // current owner's row in registers and searches again (over the
@@ -345,15 +351,17 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         const uint32_t populated = min(hi - base, static_cast<uint32_t>(kBT));
         uint32_t ow = 0, o_end = 0, o_base = 0;
         bool have = false;
-        // kBatch adjacency loads in flight per thread before any body runs.
-        // The ids are staged in shared memory (a register array indexed by a
-        // runtime k would spill) and one non-unrolled loop runs the body, so
-        // the body is instantiated once (unrolled copies overflow the
-        // instruction cache). Owner indices pack into one register (8 bits).
+        // kBatch adjacency loads in flight per thread before any body runs:
+        // all loads are issued into registers first, then one non-unrolled
+        // loop runs the body on vv[0] and shifts the batch down (the body is
+        // instantiated once: unrolled copies overflow the instruction cache;
+        // staging through shared memory would wait on each load in turn).
+        // Owner indices pack into one register (8 bits each).
         constexpr uint32_t kBatch = Store::kLoadBatch;
         static_assert(kBT <= 256 && kBatch <= 4, "owner indices pack into 32 bits");
         for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kBatch) {
             uint32_t owners = 0, cnt = 0;
+            uint32_t vv[kBatch];
 #pragma unroll
             for (uint32_t k = 0; k < kBatch; ++k) {
                 const uint32_t e = e0 + k * kBT;
@@ -370,20 +378,27 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                         o_base = sh.cbase[ow];
                         have = true;
                     }
-                    sh.stage[k][C.tid] = C.nbrs[o_base + e];
+                    vv[k] = C.nbrs[o_base + e];
                     owners |= ow << (8 * k);
                     cnt = k + 1;
                 }
             }
 #pragma unroll 1
             for (uint32_t k = 0; k < cnt; ++k) {
-                const uint32_t v = sh.stage[k][C.tid];
+                const uint32_t v = vv[0];
                 ADSB_DCHECK(v < C.n);
-                const uint32_t w = (owners >> (8 * k)) & 0xFFu;
+                const uint32_t w = owners & 0xFFu;
+                owners >>= 8;
                 body(sh.cslot[w], sh.cval[w], v);
+#pragma unroll
+                for (uint32_t j = 0; j + 1 < kBatch; ++j) vv[j] = vv[j + 1];
             }
         }
+        ADSB_PHASE_MARK(f2);
         __syncthreads();
+        ADSB_PHASE_MARK(f3);
+        ADSB_PHASE_ADD(9, f2 - f1);
+        ADSB_PHASE_ADD(11, f3 - f2);
     }
 }
 
@@ -413,6 +428,7 @@ __device__ __forceinline__ void add_degsum(Ctx& C, uint32_t my_deg, uint32_t slo
 // offset loads overlap (4 in flight per thread) instead of stalling each claim.
 template <class Store>
 __device__ uint32_t level_degrees(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, uint32_t slot) {
+    ADSB_PHASE_MARK(ld0);
     uint32_t my = 0;
     for (uint32_t i0 = lo + C.tid; i0 < hi; i0 += 4 * kBT) {
         uint32_t v[4];
@@ -432,6 +448,7 @@ __device__ uint32_t level_degrees(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bo
     }
     add_degsum(C, my, slot);
     __syncthreads();
+    ADSB_PHASE_ADD(10, clock64() - ld0);
     return C.sh->lvl_deg[slot];
 }
 
@@ -476,9 +493,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         if (deg_s <= deg_t && S.room_for(deg_s)) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
-            C.verts += C.tid == 0 ? s_hi - s_lo : 0;
+            if (C.tid == 0) sh.st_verts += s_hi - s_lo;
             bool met = false;
-            for_edges(C, S, s_lo, s_hi, false, C.edges,
+            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           bool ins;
@@ -505,7 +522,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                 return {a, b, 0};
             }
             if (!Store::kSigmaPreZeroed)
-            for_edges(C, S, s_lo, s_hi, false, C.edges,
+            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -521,10 +538,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
-            C.verts += C.tid == 0 ? t_hi - t_lo : 0;
+            if (C.tid == 0) sh.st_verts += t_hi - t_lo;
             bool met = false;
             const uint32_t meta_new = kMetaT | (b + 1);
-            for_edges(C, S, t_lo, t_hi, true, C.edges,
+            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
                           bool ins;
@@ -560,9 +577,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             deg_t = level_degrees(C, S, t_lo, t_hi, true, cur);
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
-            C.verts += C.tid == 0 ? s_hi - s_lo : 0;
+            if (C.tid == 0) sh.st_verts += s_hi - s_lo;
             bool met = false;
-            for_edges(C, S, s_lo, s_hi, false, C.edges,
+            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -576,7 +593,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (__syncthreads_or(met)) return {a, b, 0};
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
-            for_edges(C, S, s_lo, s_hi, false, C.edges,
+            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return Store::kSigmaPreZeroed ? S.sigma(slot) : 0ull; },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           bool ins;
@@ -596,7 +613,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
             if (!Store::kSigmaPreZeroed)
-            for_edges(C, S, s_lo, s_hi, false, C.edges,
+            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -611,9 +628,9 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
         } else {
             // ---- t-side level b: probe for the s-ball
-            C.verts += C.tid == 0 ? t_hi - t_lo : 0;
+            if (C.tid == 0) sh.st_verts += t_hi - t_lo;
             bool met = false;
-            for_edges(C, S, t_lo, t_hi, true, C.edges,
+            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
                           uint32_t m;
@@ -626,7 +643,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             if (__syncthreads_or(met)) return {a, b, 0};
             const uint32_t meta_new = kMetaT | (b + 1);
-            for_edges(C, S, t_lo, t_hi, true, C.edges,
+            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t, unsigned long long, uint32_t v) {
                           bool ins;
@@ -659,7 +676,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
 template <class Store>
 __device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
     for (uint32_t k = b; k >= 1; --k) {
-        for_edges(C, S, S.tlev[k - 1], S.tlev[k], true, C.rebuild_edges,
+        for_edges(C, S, S.tlev[k - 1], S.tlev[k], true, &C.sh->st_rebuild,
                   [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                   [&](uint32_t w_slot, unsigned long long, uint32_t v) {
                       uint32_t m;
@@ -747,7 +764,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                                (!want_t || (m & kMetaDag));
                         if (cand) val = S.sigma(sl);
                     }
-                    C.back_edges += C.lane == 0 ? min(32u, end - base) : 0;
+                    if (C.lane == 0) sh.st_back += min(32u, end - base);
                     const uint32_t cb = __ballot_sync(kFull, cand);
                     if (first == kNone && cb) {
                         const int f0 = __ffs(cb) - 1;
@@ -767,7 +784,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                     ch = first;
                     chm = firstm;
                     chs = 0;
-                    C.degenerate += C.lane == 0 ? 1 : 0;
+                    if (C.lane == 0) sh.st_degen += 1;
                 }
                 if (C.lane == 0) {
                     sh.first = ch;
@@ -794,7 +811,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                 if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag)))
                     val = S.sigma(sl);
             }
-            C.back_edges += C.tid == 0 ? min(static_cast<uint32_t>(kBT), end - base) : 0;
+            if (C.tid == 0) sh.st_back += min(static_cast<uint32_t>(kBT), end - base);
             // per-warp 65-bit candidate totals, then the warp whose range holds
             // r walks its candidates in lane (= id) order
             const uint32_t cb = __ballot_sync(kFull, val != 0);
@@ -880,7 +897,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                 __syncthreads();
             }
             if (!found) return false;
-            C.degenerate += C.tid == 0 ? 1 : 0;
+            if (C.tid == 0) sh.st_degen += 1;
         }
         if (C.tid == 0) {
             if (kMode == kModeDet) {
@@ -943,9 +960,41 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 
 // One sample (s, t draw + traversal + backtrack) with the shared-memory store
 // first and the global store as fallback. Returns 0 ok or an error code.
-template <int kMode, bool kGlobalOnly, class GS>
-__device__ void one_sample(Ctx& C, SmemStore& sm, GS& gs, const SamplerParams& p, SplitMix64& rng,
-                           uint32_t frame_local, unsigned long long& fallbacks, unsigned long long& errors) {
+extern __shared__ unsigned long long adsb_dyn[];
+
+// Store descriptors are rebuilt per sample from the launch parameters rather
+// than kept live across the sample loop (register budget: 64 per thread).
+__device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Shared& sh) {
+    SmemStore sm;
+    const uint32_t H = p.hash_cap;
+    sm.km = adsb_dyn;
+    sm.sig = adsb_dyn + H;
+    sm.qcap = H / 2;
+    sm.qv = reinterpret_cast<uint32_t*>(adsb_dyn + 2 * H);
+    sm.tlev = sh.tlev_small;
+    sm.mask = H - 1;
+    sm.shift = 32 - (31 - __clz(H));
+    sm.limit = H / 2;
+    sm.level_cap = kSmemLevels;
+    sm.sh = &sh;
+    return sm;
+}
+
+__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const SamplerParams& p, uint32_t tag) {
+    GlobalStoreT<ADSB_LOAD_BATCH> gs;
+    const uint32_t slot = blockIdx.x;
+    gs.st = p.state + 2ull * p.slot_stride * slot;
+    gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
+    gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
+    gs.tag = tag;
+    gs.qcap = p.n;
+    gs.level_cap = p.level_cap;
+    return gs;
+}
+
+// gtag: this block's generation tag for the global store (block-uniform).
+template <int kMode, bool kGlobalOnly>
+__device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint32_t frame_local, uint32_t& gtag) {
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
     uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
     if (t >= s) ++t;
@@ -953,14 +1002,18 @@ __device__ void one_sample(Ctx& C, SmemStore& sm, GS& gs, const SamplerParams& p
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
     int rc = 1;
     if constexpr (!kGlobalOnly) {
-        if (p.use_smem) rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+        if (p.use_smem) {
+            SmemStore sm = make_smem_store(p, *C.sh);
+            rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+        }
     }
     if (rc == 1) {
-        fallbacks += (!kGlobalOnly && p.use_smem) ? 1 : 0;
-        gs.tag += 1;
+        if (C.tid == 0 && !kGlobalOnly && p.use_smem) C.sh->n_fallbacks += 1;
+        gtag += 1;
+        auto gs = make_global_store(p, gtag);
         rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
     }
-    if (rc != 0) ++errors;
+    if (rc != 0 && C.tid == 0) C.sh->n_errors += 1;
 }
 
 __device__ __forceinline__ unsigned long long vload(const unsigned long long* a) {
@@ -1057,7 +1110,6 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
 template <int kMode, bool kGlobalOnly>
 __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     sampler_cta_kernel(SamplerParams p) {
-    extern __shared__ unsigned long long dyn[];
     __shared__ Shared sh;
     Ctx C;
     C.off = p.off;
@@ -1066,42 +1118,22 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
-    C.edges = C.rebuild_edges = C.back_edges = C.verts = C.degenerate = 0;
     C.n = p.n;
     C.low_degree = p.max_degree <= 32;
     const uint32_t slot = blockIdx.x;
+    uint32_t gtag = p.slot_tag[slot];
 
-    SmemStore sm;
-    const uint32_t H = p.hash_cap;
-    sm.km = dyn;
-    sm.sig = dyn + H;
-    sm.qcap = H / 2;
-    sm.qv = reinterpret_cast<uint32_t*>(dyn + 2 * H);
-    sm.tlev = sh.tlev_small;
-    sm.mask = H - 1;
-    sm.shift = 32 - (31 - __clz(H));
-    sm.limit = H / 2;
-    sm.level_cap = kSmemLevels;
-    sm.sh = &sh;
-
-    GlobalStoreT<ADSB_LOAD_BATCH> gs;
-    gs.st = p.state + 2ull * p.slot_stride * slot;
-    gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
-    gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
-    gs.tag = p.slot_tag[slot];
-    gs.qcap = p.n;
-    gs.level_cap = p.level_cap;
-
-    if constexpr (!kGlobalOnly) sm.clear_all(C.tid);
+    if constexpr (!kGlobalOnly) make_smem_store(p, sh).clear_all(C.tid);
     __syncthreads();
     ADSB_PHASE_MARK(k0);
-    unsigned long long samples = 0, fallbacks = 0, errors = 0;
     // The published ticket is double-buffered by loop parity: one barrier per
     // sample (slot `par` is rewritten two iterations later, after every thread
     // passed the next barrier). Tickets are not fetched ahead: a block holding
     // a second ticket through a long sample delays the tail (measured on C4).
     if (C.tid == 0) {
         sh.recorded = 0;
+        sh.st_edges = sh.st_rebuild = sh.st_back = sh.st_verts = sh.st_degen = 0;
+        sh.n_samples = sh.n_fallbacks = sh.n_errors = 0;
         sh.last_d = 0;
         sh.pending = 0;
         sh.done_old = 0;
@@ -1116,8 +1148,8 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
             const uint64_t local = item * p.world + p.rank;
             SplitMix64 rng(reseed(p.seed, p.first + local));
             for (uint64_t i = 0; i < p.spf; ++i) {
-                ++samples;
-                one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, static_cast<uint32_t>(local), fallbacks, errors);
+                if (C.tid == 0) sh.n_samples += 1;
+                one_sample<kMode, kGlobalOnly>(C, p, rng, static_cast<uint32_t>(local), gtag);
             }
         }
     } else {
@@ -1158,9 +1190,9 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
             if (item == ~0ull) break;
             const uint32_t k = static_cast<uint32_t>((item / p.epoch_b) % p.ring_k);
             SplitMix64 rng(reseed(p.seed, item));
-            ++samples;
+            if (C.tid == 0) sh.n_samples += 1;
             const uint32_t rec0 = sh.recorded;
-            one_sample<kMode, kGlobalOnly>(C, sm, gs, p, rng, k, fallbacks, errors);
+            one_sample<kMode, kGlobalOnly>(C, p, rng, k, gtag);
             if (C.tid == 0) {
                 if (p.audit && item < p.max_epochs * p.epoch_b)
                     p.audit[item] = (sh.recorded - rec0) | (sh.last_d << 16);
@@ -1172,16 +1204,18 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     }
     ADSB_PHASE_MARK(k1);
     ADSB_PHASE_ADD(4, k1 - k0);
-    // per-thread counters: reduce across the block once
-    atomicAdd(p.stats + kStatEdges, C.edges + C.rebuild_edges + C.back_edges);
-    atomicAdd(p.stats + kStatRebuildEdges, C.rebuild_edges);
-    atomicAdd(p.stats + kStatBacktrackEdges, C.back_edges);
-    atomicAdd(p.stats + kStatVertices, C.verts);
+    __syncthreads();  // low-degree expansions add edge counts from every warp
     if (C.tid == 0) {
-        p.slot_tag[slot] = gs.tag;
-        atomicAdd(p.stats + kStatSamples, samples);
-        atomicAdd(p.stats + kStatFallbacks, fallbacks);
-        if (errors) atomicAdd(p.stats + kStatErrors, errors);
-        if (C.degenerate) atomicAdd(p.stats + kStatDegenerate, C.degenerate);
+        atomicAdd(p.stats + kStatEdges, sh.st_edges + sh.st_rebuild + sh.st_back);
+        atomicAdd(p.stats + kStatRebuildEdges, sh.st_rebuild);
+        atomicAdd(p.stats + kStatBacktrackEdges, sh.st_back);
+        atomicAdd(p.stats + kStatVertices, sh.st_verts);
+    }
+    if (C.tid == 0) {
+        p.slot_tag[slot] = gtag;
+        atomicAdd(p.stats + kStatSamples, sh.n_samples);
+        atomicAdd(p.stats + kStatFallbacks, sh.n_fallbacks);
+        if (sh.n_errors) atomicAdd(p.stats + kStatErrors, sh.n_errors);
+        if (sh.st_degen) atomicAdd(p.stats + kStatDegenerate, sh.st_degen);
     }
 }
