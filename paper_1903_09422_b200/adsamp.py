@@ -203,6 +203,7 @@ class Graph:
         self._h = handle
         n = C.c_uint32()
         nnz = C.c_uint64()
+        self._destroy = lib().adsb_graph_destroy
         check(lib().adsb_graph_info(self._h, C.byref(n), C.byref(nnz)))
         self._n = n.value
         self._nnz = nnz.value
@@ -210,8 +211,9 @@ class Graph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().adsb_graph_destroy(h)
+        destroy = getattr(self, "_destroy", None)
+        if h and destroy is not None:  # bound at construction: module globals may be gone at exit
+            destroy(h)
             self._h = None
 
     @property

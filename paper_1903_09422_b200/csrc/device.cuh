@@ -88,7 +88,7 @@ struct PinnedBuf {
 enum class Scratch : int {
     kParent, kIsRoot, kRank, kCubTemp, kFlags, kDist, kFrontA, kFrontB, kLevelCounts, kBest,
     kTotal, kStats, kScal, kBaseMax, kStopIdx, kEvents, kSorted, kGathered, kFrameMax, kRunMax,
-    kSortTemp, kEpochCnt, kDmax, kFlagDev, kTickets, kNcclScalar, kCtl, kRingCnt, kRingList, kRingLen, kEvents2, kScal2, kAudit, kCount
+    kSortTemp, kEpochCnt, kDmax, kFlagDev, kTickets, kNcclScalar, kCtl, kRingCnt, kRingList, kRingLen, kEvents2, kScal2, kAudit, kMode, kCount
 };
 
 struct ScratchPool {

@@ -7,7 +7,9 @@
 //
 // Components: lock-free union-find hooking (larger root -> smaller root), so
 // every root is its component's smallest vertex; ranking the roots in id
-// order then reproduces the reference's DFS numbering exactly.
+// order then reproduces the reference's DFS numbering exactly. Edges are
+// linked Afforest-style: two sampled neighbours per vertex first, then the
+// full adjacency only of vertices outside the (sampled) giant component.
 // D_ub: one multi-source, level-synchronous BFS from every component's
 // max-degree vertex (lowest id on ties); the deepest level is the largest
 // eccentricity, D_ub = 2 * that.
@@ -25,18 +27,21 @@ namespace {
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 
-// Parent pointers only ever decrease (hooks link the larger root below the
-// smaller; halving skips to a smaller ancestor). Every pointer write is an
-// atomicMin so a thread holding a stale read can never raise one again: with
-// plain stores, a late halving write could overwrite uf_compress's
-// parent[v] = root with a non-root ancestor and mislabel v.
+// Root with path halving. Parent pointers only ever decrease (hooks link the
+// larger root below the smaller; halving skips to a smaller ancestor), and a
+// racing halving write always stores an ancestor, so connectivity is safe
+// with plain stores while hooking. uf_compress needs kMonotone: there a late
+// plain halving write could overwrite parent[v] = root with a non-root
+// ancestor and mislabel v, so every write is an atomicMin.
+template <bool kMonotone>
 __device__ __forceinline__ uint32_t uf_root(uint32_t* parent, uint32_t v) {
     volatile uint32_t* p = parent;
     uint32_t cur = p[v];
     if (cur != v) {
         uint32_t prev = v, next;
-        while (cur > (next = p[cur])) {  // path halving
-            atomicMin(parent + prev, next);
+        while (cur > (next = p[cur])) {
+            if (kMonotone) atomicMin(parent + prev, next);
+            else p[prev] = next;
             prev = cur;
             cur = next;
         }
@@ -49,32 +54,64 @@ __global__ void uf_init(uint32_t* parent, uint32_t n) {
         parent[v] = v;
 }
 
-// one warp per vertex, lanes over its neighbours; each undirected edge once (u < w)
-__global__ void uf_hook(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs,
-                        uint32_t* parent, uint32_t n) {
+// Union of the trees holding u and w: hook the larger root below the smaller
+// (roots stay the smallest id of their component).
+__device__ __forceinline__ void uf_link(uint32_t* parent, uint32_t u, uint32_t w) {
+    uint32_t ru = uf_root<false>(parent, u), rw = uf_root<false>(parent, w);
+    while (ru != rw) {
+        const uint32_t hi = max(ru, rw), lo = min(ru, rw);
+        const uint32_t old = atomicCAS(&parent[hi], hi, lo);
+        if (old == hi) break;
+        ru = uf_root<false>(parent, old);
+        rw = uf_root<false>(parent, lo);
+    }
+}
+
+// Afforest-style sampling: round r links every vertex to its r-th neighbour.
+// Two rounds already join nearly all of a giant component.
+__global__ void uf_link_round(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs, uint32_t* parent,
+                              uint32_t n, uint32_t r) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const uint32_t b = off[v];
+        if (off[v + 1] - b > r) uf_link(parent, v, nbrs[b + r]);
+    }
+}
+
+// The most frequent root among 256 evenly spaced vertices (one block).
+__global__ void uf_sample_mode(uint32_t* parent, uint32_t n, uint32_t* mode) {
+    __shared__ uint32_t roots[256];
+    __shared__ unsigned long long best;
+    const uint32_t i = threadIdx.x;
+    const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(i) * n) / 256);
+    roots[i] = uf_root<false>(parent, min(v, n - 1));
+    if (i == 0) best = 0;
+    __syncthreads();
+    uint32_t count = 0;
+    for (uint32_t j = 0; j < 256; ++j) count += roots[j] == roots[i] ? 1u : 0u;
+    atomicMax(&best, (static_cast<unsigned long long>(count) << 32) | roots[i]);
+    __syncthreads();
+    if (i == 0) *mode = static_cast<uint32_t>(best);
+}
+
+// The rest of the edges, only for vertices outside the sampled giant tree:
+// one warp per vertex, lanes over its adjacency beyond the two sampled
+// entries (an edge into the giant is seen from the outside endpoint).
+__global__ void uf_link_rest(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs, uint32_t* parent,
+                             uint32_t n, const uint32_t* mode) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t giant = *mode;
     for (uint32_t u = warp; u < n; u += nwarps) {
+        if (uf_root<false>(parent, u) == giant) continue;  // warp-uniform
         const uint32_t b = off[u], e = off[u + 1];
-        for (uint32_t i = b + lane; i < e; i += 32) {
-            const uint32_t w = nbrs[i];
-            if (w < u) continue;
-            uint32_t ru = uf_root(parent, u), rw = uf_root(parent, w);
-            while (ru != rw) {
-                const uint32_t hi = max(ru, rw), lo = min(ru, rw);
-                const uint32_t old = atomicCAS(&parent[hi], hi, lo);
-                if (old == hi) break;
-                ru = uf_root(parent, old);
-                rw = uf_root(parent, lo);
-            }
-        }
+        for (uint32_t i = b + 2 + lane; i < e; i += 32) uf_link(parent, u, nbrs[i]);
     }
 }
 
 __global__ void uf_compress(uint32_t* parent, uint32_t* is_root, uint32_t n) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const uint32_t r = uf_root(parent, v);  // hooking is complete: r is final
+        const uint32_t r = uf_root<true>(parent, v);  // hooking is complete: r is final
         atomicMin(parent + v, r);
         is_root[v] = r == v ? 1u : 0u;
     }
@@ -88,10 +125,28 @@ __global__ void uf_label(const uint32_t* parent, const uint32_t* root_rank, uint
 // graph.hpp:208: start = max degree, lowest id on ties -> max of (deg, ~v)
 __global__ void argmax_degree(const uint32_t* __restrict__ off, const uint32_t* __restrict__ label,
                               unsigned long long* best, uint32_t n) {
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const unsigned long long key =
-            (static_cast<unsigned long long>(off[v + 1] - off[v]) << 32) | static_cast<uint32_t>(~v);
-        atomicMax(&best[label[v]], key);
+    // grid-stride with whole warps (n rounded up) so the warp reduction below
+    // always has every lane present; one atomic per warp when the warp's
+    // vertices share a component (the common case: one giant component)
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t span = (n + 31u) & ~31u;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < span; v += stride) {
+        const bool live = v < n;
+        const uint32_t lab = live ? label[v] : 0xFFFFFFFFu;
+        unsigned long long key = live ? (static_cast<unsigned long long>(off[v + 1] - off[v]) << 32) |
+                                            static_cast<uint32_t>(~v)
+                                      : 0ull;
+        const uint32_t lab0 = __shfl_sync(0xFFFFFFFFu, lab, 0);
+        if (__all_sync(0xFFFFFFFFu, lab == lab0 || !live)) {
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xFFFFFFFFu, key, d);
+                key = o > key ? o : key;
+            }
+            if ((threadIdx.x & 31) == 0 && lab0 != 0xFFFFFFFFu) atomicMax(&best[lab0], key);
+        } else if (live) {
+            atomicMax(&best[lab], key);
+        }
     }
 }
 
@@ -216,7 +271,7 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
     dg.n = g.n;
     dg.nnz = g.nnz();
     // u32 offsets on the device: narrow on the host, then one copy each.
-    std::vector<uint32_t> off32(g.offsets.size());
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> off32(g.offsets.size());  // page-locked when large
     for (size_t i = 0; i < off32.size(); ++i) off32[i] = static_cast<uint32_t>(g.offsets[i]);
     for (uint32_t u = 0; u < g.n; ++u) dg.max_degree = std::max<uint32_t>(dg.max_degree, off32[u + 1] - off32[u]);
     dg.offsets = take_buffer(*ctx->rt, off32.size());
@@ -246,9 +301,12 @@ uint32_t device_components(DeviceContext& ctx) {
     uint32_t* rank = ctx.rt->pool.get<uint32_t>(Scratch::kRank, n + 1);
     if (ctx.labels.count < n) ctx.labels = take_buffer(*ctx.rt, n);
     const unsigned g = grid_for(n, ctx.device);
+    uint32_t* mode = ctx.rt->pool.get<uint32_t>(Scratch::kMode, 1);
     uf_init<<<g, 256, 0, s>>>(parent, n);
-    uf_hook<<<grid_for(static_cast<uint64_t>(n) * 32, ctx.device), 256, 0, s>>>(
-        ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent, n);
+    for (uint32_t r = 0; r < 2; ++r) uf_link_round<<<g, 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent, n, r);
+    uf_sample_mode<<<1, 256, 0, s>>>(parent, n, mode);
+    uf_link_rest<<<grid_for(static_cast<uint64_t>(n) * 32, ctx.device), 256, 0, s>>>(
+        ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, parent, n, mode);
     uf_compress<<<g, 256, 0, s>>>(parent, is_root, n);
     ADSB_CUDA(cudaMemsetAsync(is_root + n, 0, sizeof(uint32_t), s));
     size_t temp_bytes = 0;
@@ -273,7 +331,7 @@ static uint64_t bfs_depth(DeviceContext& ctx, uint32_t* dist, uint32_t* fa, uint
     const uint32_t n = ctx.graph.n;
     cudaStream_t s = ctx.rt->stream;
     const unsigned grid = static_cast<unsigned>(num_sms(ctx.device) * 8);
-    constexpr uint32_t kChunk = 32;
+    uint32_t kChunk = 8;  // levels launched per host check: 8 first, then 32
     uint32_t level = 0;
     uint32_t* host = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr);  // 64 words of pinned staging
     for (;;) {
@@ -293,6 +351,7 @@ static uint64_t bfs_depth(DeviceContext& ctx, uint32_t* dist, uint32_t* fa, uint
             if (host[k] == 0) return level + k;
         level += avail;
         if (level >= n) return level;
+        kChunk = 32;
     }
 }
 

@@ -14,10 +14,16 @@
 // than the reference's single global sort; the result is identical.
 #include "graph_host.hpp"
 
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
 #include <fstream>
 #include <numeric>
 #include <set>
@@ -34,6 +40,69 @@ unsigned host_threads() {
     return hw == 0 ? 1 : std::min(hw, 64u);
 }
 
+namespace {
+
+struct HostBlockCache {
+    std::mutex mu;
+    std::map<size_t, std::vector<void*>> free;  // size class (power of two) -> blocks
+    size_t cached = 0;
+    int pinned = -1;  // -1 unknown, 0 malloc, 1 cudaHostAlloc
+    static constexpr size_t kCap = size_t{2} << 30;
+};
+
+HostBlockCache& host_cache() {
+    static HostBlockCache* c = new HostBlockCache();  // never destroyed: blocks may outlive statics
+    return *c;
+}
+
+size_t size_class(size_t bytes) {
+    size_t c = kHostBlockMin;
+    while (c < bytes) c <<= 1;
+    return c;
+}
+
+}  // namespace
+
+void* host_block_alloc(size_t bytes) {
+    HostBlockCache& c = host_cache();
+    const size_t cls = size_class(bytes);
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.free.find(cls);
+    if (it != c.free.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        c.cached -= cls;
+        return p;
+    }
+    if (c.pinned < 0) {
+        int count = 0;
+        c.pinned = cudaGetDeviceCount(&count) == cudaSuccess && count > 0 ? 1 : 0;
+        cudaGetLastError();
+    }
+    void* p = nullptr;
+    if (c.pinned == 1 && cudaHostAlloc(&p, cls, cudaHostAllocPortable) == cudaSuccess) return p;
+    cudaGetLastError();
+    p = std::malloc(cls);
+    if (!p) throw std::bad_alloc();
+    return p;
+}
+
+void host_block_free(void* p, size_t bytes) noexcept {
+    if (!p) return;
+    HostBlockCache& c = host_cache();
+    const size_t cls = size_class(bytes);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (c.cached + cls <= HostBlockCache::kCap) {
+        c.free[cls].push_back(p);
+        c.cached += cls;
+        return;
+    }
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost) cudaFreeHost(p);
+    else std::free(p);
+    cudaGetLastError();
+}
+
 template <class F>
 static void parallel_for(uint64_t count, F&& body) {
     const unsigned T = host_threads();
@@ -47,6 +116,36 @@ static void parallel_for(uint64_t count, F&& body) {
         const uint64_t b = t * chunk, e = std::min(count, b + chunk);
         if (b >= e) break;
         th.emplace_back([&, b, e] { body(b, e); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// parallel_for over vertices [0, n) with ranges of about equal adjacency
+// volume (offsets: n+1 prefix sums).
+template <class F>
+static void parallel_for_weighted(uint64_t n, const uint64_t* offsets, F&& body) {
+    const unsigned T = host_threads();
+    const uint64_t total = offsets[n] + n;  // + n: every vertex costs something
+    if (total < 262144 || T == 1) {
+        body(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    uint64_t b = 0;
+    for (unsigned t = 0; t < T && b < n; ++t) {
+        uint64_t e = n;
+        if (t + 1 < T) {
+            const uint64_t target = total * (t + 1) / T;
+            uint64_t lo = b, hi = n;  // first vertex u with offsets[u] + u >= target
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if (offsets[mid] + mid < target) lo = mid + 1;
+                else hi = mid;
+            }
+            e = std::max(lo, b + 1);
+        }
+        th.emplace_back([&, b, e] { body(b, e); });
+        b = e;
     }
     for (auto& x : th) x.join();
 }
@@ -106,7 +205,8 @@ HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nb
     g.nbrs.resize(offsets[n]);
     std::atomic<bool> bad{false};
     // one parallel pass: copy each vertex range and check the Graph invariants
-    parallel_for(n, [&](uint64_t b, uint64_t e) {
+    // (ranges split by adjacency volume: hubs make vertex-count splits uneven)
+    parallel_for_weighted(n, offsets, [&](uint64_t b, uint64_t e) {
         std::memcpy(g.offsets.data() + b, offsets + b, (e - b) * sizeof(uint64_t));
         std::memcpy(g.nbrs.data() + offsets[b], nbrs + offsets[b], (offsets[e] - offsets[b]) * sizeof(uint32_t));
         bool local_bad = false;

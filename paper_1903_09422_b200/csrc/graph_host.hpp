@@ -15,6 +15,14 @@
 
 namespace adsb {
 
+// Large host blocks (>= kHostBlockMin bytes) come from a process-wide cache:
+// page-locked when a CUDA device is present (the device upload is then a
+// direct DMA), plain malloc otherwise; freed blocks are kept for reuse
+// (bounded), so building graphs repeatedly does not re-fault or re-pin pages.
+constexpr size_t kHostBlockMin = size_t{256} << 10;
+void* host_block_alloc(size_t bytes);
+void host_block_free(void* p, size_t bytes) noexcept;
+
 // Allocator that leaves trivially-constructible elements uninitialised on
 // resize: large CSR arrays are filled by parallel copies right after.
 template <class T>
@@ -27,6 +35,20 @@ struct NoInitAlloc : std::allocator<T> {
     NoInitAlloc() = default;
     template <class U>
     NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    T* allocate(size_t count) {
+        const size_t bytes = count * sizeof(T);
+        if (bytes >= kHostBlockMin) return static_cast<T*>(host_block_alloc(bytes));
+        return std::allocator<T>::allocate(count);
+    }
+    void deallocate(T* p, size_t count) noexcept {
+        const size_t bytes = count * sizeof(T);
+        if (bytes >= kHostBlockMin) host_block_free(p, bytes);
+        else std::allocator<T>::deallocate(p, count);
+    }
+    template <class U>
+    bool operator==(const NoInitAlloc<U>&) const noexcept { return true; }
+    template <class U>
+    bool operator!=(const NoInitAlloc<U>&) const noexcept { return false; }
     template <class U>
     void construct(U*) noexcept {}
     template <class U, class... A>
