@@ -120,14 +120,16 @@ struct SamplerArena {
     int kind = 1;            // SamplerKind (0 warp teams, 1 block teams)
     uint32_t hash_cap = 0;   // block teams: shared-memory hash capacity
     uint32_t block_threads = 256;
-    uint32_t slots = 0;
+    uint32_t slots = 0;      // warp teams; block teams: global-state regions
+    uint32_t blocks = 0;     // block teams: resident blocks launched by the shared-memory kernels
     uint32_t n = 0;
     uint32_t level_cap = 0;
     DevBuf<unsigned long long> state;  // slots * n * 2 (meta, sigma)
     DevBuf<uint32_t> queue;            // slots * n
     DevBuf<uint2> qrange;              // slots * n (offset, degree)
     DevBuf<uint32_t> tlev;             // slots * level_cap
-    DevBuf<uint32_t> slot_tag;         // slots
+    DevBuf<uint32_t> slot_tag;         // slots: generation tag of each region
+    DevBuf<uint32_t> slot_busy;        // block teams: bitmap of regions lent to blocks
 };
 
 // Process-wide per-device runtime shared by every graph handle on that

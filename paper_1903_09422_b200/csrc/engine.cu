@@ -196,10 +196,12 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
                                                   : std::max(sampler_cta_blocks_per_sm(hash_cap, block_threads), 1);
     size_t free_b = 0, total_b = 0;
     ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t per_slot = static_cast<uint64_t>(cap_n) * (16 + 4 + 8) + static_cast<uint64_t>(cap_levels) * 4;
+    // per region: state (16 B/vertex), queue (4), warp teams also ranges (8)
+    const uint64_t per_vertex = kind == SamplerKind::kWarp ? 16 + 4 + 8 : 16 + 4;
+    const uint64_t per_slot = static_cast<uint64_t>(cap_n) * per_vertex + static_cast<uint64_t>(cap_levels) * 4;
     const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
-    uint64_t slots = static_cast<uint64_t>(sms) * per_sm;
-    slots = std::min<uint64_t>(slots, budget / std::max<uint64_t>(per_slot, 1));
+    const uint64_t resident = static_cast<uint64_t>(sms) * per_sm;
+    uint64_t slots = std::min<uint64_t>(resident, budget / std::max<uint64_t>(per_slot, 1));
     if (kind == SamplerKind::kWarp) slots = slots / 8 * 8;
     if (slots < (kind == SamplerKind::kWarp ? 8u : 1u))
         fail(ADSB_ERR_CUDA, "not enough device memory for the sampler scratch (" +
@@ -209,13 +211,19 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->hash_cap = hash_cap;
     a->block_threads = block_threads;
     a->slots = static_cast<uint32_t>(slots);
+    // Block teams launch every resident block for the shared-memory kernels
+    // even when fewer global regions fit (huge graphs): a sample that
+    // overflows the table borrows a free region for its redo.
+    a->blocks = kind == SamplerKind::kWarp ? a->slots : static_cast<uint32_t>(resident);
     a->n = cap_n;
     a->level_cap = cap_levels;
     a->state.alloc(slots * cap_n * 2);
     a->queue.alloc(slots * cap_n);
-    a->qrange.alloc(slots * cap_n);
+    if (kind == SamplerKind::kWarp) a->qrange.alloc(slots * cap_n);
     a->tlev.alloc(slots * cap_levels);
     a->slot_tag.alloc(slots);
+    a->slot_busy.alloc((slots + 31) / 32);
+    ADSB_CUDA(cudaMemsetAsync(a->slot_busy.ptr, 0, a->slot_busy.bytes(), rt.stream));
     ADSB_CUDA(cudaMemsetAsync(a->state.ptr, 0, a->state.bytes(), rt.stream));
     ADSB_CUDA(cudaMemsetAsync(a->slot_tag.ptr, 0, a->slot_tag.bytes(), rt.stream));
     ADSB_CUDA(cudaStreamSynchronize(rt.stream));
@@ -242,6 +250,8 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.qrange = a.qrange.ptr;
     p.tlev = a.tlev.ptr;
     p.slot_tag = a.slot_tag.ptr;
+    p.slot_busy = a.slot_busy.ptr;
+    p.blocks = a.blocks;
     p.hash_cap = a.hash_cap;
     p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
     p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
@@ -357,7 +367,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (trace_enabled())
         std::fprintf(stderr, "[adsb] preprocess: components %.3f ms, D_ub %.3f ms, arena %.3f ms (kind %d, slots %u)\n",
                      1e3 * t_cc, 1e3 * (t_dub - t_cc), 1e3 * (out.preprocess_seconds - t_dub), arena(ctx).kind,
-                     arena(ctx).slots);
+                     arena(ctx).kind == 0 ? arena(ctx).slots : arena(ctx).blocks);
 
     Timer ads;
     const RuleParams rule{out.omega, static_cast<double>(out.omega), log_inv, eps};
@@ -374,7 +384,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     cudaEvent_t e0 = ctx.rt->ev_a, e1 = ctx.rt->ev_b;
     Launches L;
     // work units that keep every team busy: warps are many and light, blocks few and heavy
-    const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).slots;
+    const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).blocks;
 
     if (opt.deterministic && !opt.comm && std::getenv("ADSB_DET_PIPELINE")) {
         // ---- deterministic frames, pipelined: while the host reads batch b's

@@ -70,6 +70,8 @@ struct SamplerParams {
     uint2* qrange;              // slots * n
     uint32_t* tlev;             // slots * level_cap
     uint32_t* slot_tag;         // slots
+    uint32_t* slot_busy;        // block teams: region bitmap (fallback samples borrow a region)
+    uint32_t blocks;            // block teams: shared-memory kernel grid
     // deterministic output: (v << 32) | frame-in-batch
     unsigned long long* events;
     unsigned long long* ev_cursor;

@@ -147,11 +147,11 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
         return;
     }
     if (p.block_threads == 128) {
-        if (deterministic) bt128::sampler_cta_kernel<kModeDet, false><<<p.slots, 128, dyn, stream>>>(p);
-        else bt128::sampler_cta_kernel<kModeEpoch, false><<<p.slots, 128, dyn, stream>>>(p);
+        if (deterministic) bt128::sampler_cta_kernel<kModeDet, false><<<p.blocks, 128, dyn, stream>>>(p);
+        else bt128::sampler_cta_kernel<kModeEpoch, false><<<p.blocks, 128, dyn, stream>>>(p);
     } else {
-        if (deterministic) bt256::sampler_cta_kernel<kModeDet, false><<<p.slots, 256, dyn, stream>>>(p);
-        else bt256::sampler_cta_kernel<kModeEpoch, false><<<p.slots, 256, dyn, stream>>>(p);
+        if (deterministic) bt256::sampler_cta_kernel<kModeDet, false><<<p.blocks, 256, dyn, stream>>>(p);
+        else bt256::sampler_cta_kernel<kModeEpoch, false><<<p.blocks, 256, dyn, stream>>>(p);
     }
     ADSB_CUDA(cudaGetLastError());
 }
@@ -164,8 +164,8 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
         ADSB_CUDA(cudaGetLastError());
         return;
     }
-    if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused, false><<<p.slots, 128, dyn, stream>>>(p);
-    else bt256::sampler_cta_kernel<kModeFused, false><<<p.slots, 256, dyn, stream>>>(p);
+    if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused, false><<<p.blocks, 128, dyn, stream>>>(p);
+    else bt256::sampler_cta_kernel<kModeFused, false><<<p.blocks, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
 }
 

@@ -28,6 +28,7 @@ struct Shared {
     unsigned long long done_old;      // thread 0 (fused): Done counter before the last sample's increment
     unsigned long long st_edges, st_rebuild, st_back, st_verts, st_degen;  // block statistics (thread 0 adds)
     unsigned long long n_samples, n_fallbacks, n_errors;
+    uint32_t g_region, g_tag;         // fallback: borrowed global region and its tag
     uint32_t pending;                 // thread 0 (fused): done_old belongs to an unprocessed completion
     uint32_t recorded, last_d;        // thread 0: increments recorded / last distance (fused audit)
     uint32_t lvl_cnt[3];              // per BFS level (slot = level % 3): vertices claimed,
@@ -980,9 +981,9 @@ __device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Sha
     return sm;
 }
 
-__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const SamplerParams& p, uint32_t tag) {
+__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const SamplerParams& p, uint32_t slot,
+                                                                           uint32_t tag) {
     GlobalStoreT<ADSB_LOAD_BATCH> gs;
-    const uint32_t slot = blockIdx.x;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
@@ -992,7 +993,37 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const
     return gs;
 }
 
-// gtag: this block's generation tag for the global store (block-uniform).
+// Borrow a free global-state region (thread 0; shared-memory kernels, whose
+// grid can exceed the number of regions on huge graphs). Spins while every
+// region is lent: holders finish their sample without waiting on anything.
+__device__ uint32_t acquire_region(const SamplerParams& p) {
+    const uint32_t words = (p.slots + 31) / 32;
+    for (uint32_t round = 0;; ++round) {
+        for (uint32_t w0 = 0; w0 < words; ++w0) {
+            const uint32_t w = (blockIdx.x + w0) % words;
+            uint32_t free_bits = ~*reinterpret_cast<volatile uint32_t*>(p.slot_busy + w);
+            if (w == words - 1 && (p.slots & 31)) free_bits &= (1u << (p.slots & 31)) - 1u;
+            while (free_bits) {
+                const uint32_t j = __ffs(free_bits) - 1;
+                const uint32_t bit = 1u << j;
+                if (!(atomicOr(p.slot_busy + w, bit) & bit)) {
+                    __threadfence();
+                    return w * 32 + j;
+                }
+                free_bits &= ~bit;
+            }
+        }
+        __nanosleep(256);
+    }
+}
+
+__device__ void release_region(const SamplerParams& p, uint32_t region, uint32_t tag) {
+    p.slot_tag[region] = tag;
+    __threadfence();
+    atomicAnd(p.slot_busy + region / 32, ~(1u << (region & 31)));
+}
+
+// gtag: the global-only kernel's generation tag for its own region (block-uniform).
 template <int kMode, bool kGlobalOnly>
 __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint32_t frame_local, uint32_t& gtag) {
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
@@ -1008,10 +1039,26 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
         }
     }
     if (rc == 1) {
-        if (C.tid == 0 && !kGlobalOnly && p.use_smem) C.sh->n_fallbacks += 1;
-        gtag += 1;
-        auto gs = make_global_store(p, gtag);
+        uint32_t region = blockIdx.x, tag;
+        if constexpr (kGlobalOnly) {
+            tag = ++gtag;
+        } else {
+            Shared& sh = *C.sh;
+            if (C.tid == 0) {
+                sh.n_fallbacks += 1;
+                sh.g_region = acquire_region(p);
+                sh.g_tag = __ldcg(p.slot_tag + sh.g_region) + 1u;
+            }
+            __syncthreads();
+            region = sh.g_region;
+            tag = sh.g_tag;
+        }
+        auto gs = make_global_store(p, region, tag);
         rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
+        if constexpr (!kGlobalOnly) {
+            __syncthreads();  // every thread is done with the region
+            if (C.tid == 0) release_region(p, region, tag);
+        }
     }
     if (rc != 0 && C.tid == 0) C.sh->n_errors += 1;
 }
@@ -1121,7 +1168,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     C.n = p.n;
     C.low_degree = p.max_degree <= 32;
     const uint32_t slot = blockIdx.x;
-    uint32_t gtag = p.slot_tag[slot];
+    uint32_t gtag = kGlobalOnly ? p.slot_tag[slot] : 0u;  // shared-memory kernels borrow regions instead
 
     if constexpr (!kGlobalOnly) make_smem_store(p, sh).clear_all(C.tid);
     __syncthreads();
@@ -1212,7 +1259,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
         atomicAdd(p.stats + kStatVertices, sh.st_verts);
     }
     if (C.tid == 0) {
-        p.slot_tag[slot] = gtag;
+        if (kGlobalOnly) p.slot_tag[slot] = gtag;
         atomicAdd(p.stats + kStatSamples, sh.n_samples);
         atomicAdd(p.stats + kStatFallbacks, sh.n_fallbacks);
         if (sh.n_errors) atomicAdd(p.stats + kStatErrors, sh.n_errors);

@@ -16,5 +16,6 @@ for i in range(reps):
     r = estimate_bc(g, w.epsilon, w.delta, cfg)
     print(f"{name} rep {i}: tau={r.tau} total={r.run.total_samples} ads={r.ads_seconds:.4f}s "
           f"wall={time.perf_counter()-t:.4f}s sampler_ms={r.sampler_ms:.2f} launches={r.kernel_launches} "
-          f"E={r.edges_scanned} (rebuild {r.rebuild_edges}, backtrack {r.backtrack_edges}) V={r.vertices_expanded}",
+          f"E={r.edges_scanned} (rebuild {r.rebuild_edges}, backtrack {r.backtrack_edges}) V={r.vertices_expanded} "
+          f"fallbacks={r.store_fallbacks}",
           flush=True)
