@@ -152,6 +152,18 @@ def run_reference(args, world: int, rank: int) -> None:
 CPU_SAMPLES_PER_CORE = {"c1_er": 2000, "c2_rmat18": 100, "c3_ba": 20, "c4_grid": 30, "c5_rmat24": 1}
 
 
+def _kernel_label(n: int, variant, diameter_bound: int, world: int) -> str:
+    """The sampler kernel the engine dispatches for this workload (engine.cu ensure_arena /
+    estimate_bc): warp teams for n <= 2^16, else block teams; the fused epoch pipeline for
+    cumulative epochs on one GPU; the global-state variant when D_ub > 128."""
+    from paper_1903_09422_b200 import adsamp
+    if n <= (1 << 16):
+        return "sampler_kernel (warp teams, global state)"
+    mode = "det" if variant == adsamp.Variant.indexed else ("fused" if world == 1 else "epoch")
+    store = "global-state" if diameter_bound > 128 else "shared-memory hash"
+    return f"sampler_cta_kernel<{mode}> (block teams, {store})"
+
+
 def cpu_baseline(w, path) -> dict:
     import oracle
     cores = os.cpu_count() or 1
@@ -329,7 +341,8 @@ def main() -> None:
         "edge_read_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": "sampler_kernel<det|epoch> (K1/K2)", "peak_source": peak_src,
+                     "kernel": _kernel_label(g.num_vertices(), variant, r0.diameter_bound, world),
+                     "peak_source": peak_src,
                      "alg_bytes_per_sample": alg_bytes / max(1, sum(r.run.total_samples for r in results)),
                      "sampler_ms_per_step": sampler_ms / args.steps,
                      "edges_per_sample": {k: v / max(1, sum(r.run.total_samples for r in results)) for k, v in {
