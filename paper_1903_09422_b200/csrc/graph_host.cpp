@@ -150,31 +150,48 @@ static void parallel_for_weighted(uint64_t n, const uint64_t* offsets, F&& body)
     for (auto& x : th) x.join();
 }
 
+
 HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
     HostGraph g;
     g.n = n;
+    // degree count and scatter on all host threads (relaxed atomic counters:
+    // the order inside a list is irrelevant, every list is sorted next)
+    std::atomic<bool> out_of_range{false};
     std::vector<uint64_t> deg(static_cast<size_t>(n) + 1, 0);
-    for (uint64_t i = 0; i < m; ++i) {
-        const uint32_t u = edges[2 * i], v = edges[2 * i + 1];
-        if (u == v) continue;
-        if (u >= n || v >= n) invalid("edge endpoint out of range");
-        deg[u + 1]++;
-        deg[v + 1]++;
-    }
-    for (uint32_t u = 0; u < n; ++u) deg[u + 1] += deg[u];
-    std::vector<uint32_t> raw(deg[n]);
-    {
-        std::vector<uint64_t> cur(deg.begin(), deg.end() - 1);
-        for (uint64_t i = 0; i < m; ++i) {
+    parallel_for(m, [&](uint64_t b, uint64_t e) {
+        bool bad = false;
+        for (uint64_t i = b; i < e; ++i) {
             const uint32_t u = edges[2 * i], v = edges[2 * i + 1];
             if (u == v) continue;
-            raw[cur[u]++] = v;
-            raw[cur[v]++] = u;
+            if (u >= n || v >= n) {
+                bad = true;
+                continue;
+            }
+            __atomic_fetch_add(&deg[u + 1], 1, __ATOMIC_RELAXED);
+            __atomic_fetch_add(&deg[v + 1], 1, __ATOMIC_RELAXED);
         }
+        if (bad) out_of_range = true;
+    });
+    if (out_of_range) invalid("edge endpoint out of range");
+    for (uint32_t u = 0; u < n; ++u) deg[u + 1] += deg[u];
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> raw(deg[n]);
+    {
+        // each thread owns a vertex range of about equal volume and streams
+        // the whole edge list, writing only its own lists (no shared cursors:
+        // hub counters bounced between cores with atomics)
+        std::vector<uint64_t> cur(deg.begin(), deg.end() - 1);
+        parallel_for_weighted(n, deg.data(), [&](uint64_t vb, uint64_t ve) {
+            for (uint64_t i = 0; i < m; ++i) {
+                const uint32_t u = edges[2 * i], v = edges[2 * i + 1];
+                if (u == v) continue;
+                if (u >= vb && u < ve) raw[cur[u]++] = v;
+                if (v >= vb && v < ve) raw[cur[v]++] = u;
+            }
+        });
     }
     // sort + unique each list in place; record the deduplicated degree
     std::vector<uint64_t> kept(static_cast<size_t>(n) + 1, 0);
-    parallel_for(n, [&](uint64_t b, uint64_t e) {
+    parallel_for_weighted(n, deg.data(), [&](uint64_t b, uint64_t e) {
         for (uint64_t u = b; u < e; ++u) {
             uint32_t* first = raw.data() + deg[u];
             uint32_t* last = raw.data() + deg[u + 1];
@@ -184,7 +201,7 @@ HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
     });
     for (uint32_t u = 0; u < n; ++u) kept[u + 1] += kept[u];
     g.nbrs.resize(kept[n]);
-    parallel_for(n, [&](uint64_t b, uint64_t e) {
+    parallel_for_weighted(n, kept.data(), [&](uint64_t b, uint64_t e) {
         for (uint64_t u = b; u < e; ++u)
             std::memcpy(g.nbrs.data() + kept[u], raw.data() + deg[u],
                         (kept[u + 1] - kept[u]) * sizeof(uint32_t));
@@ -289,16 +306,22 @@ HostGraph finish(Interner& in, const std::vector<uint32_t>& edges) {
 
 }  // namespace
 
-HostGraph parse_edge_list_text(const char* text, uint64_t len) {
-    Interner in;
-    std::vector<uint32_t> edges;
-    const char* p = text;
-    const char* end = text + len;
-    uint64_t line_no = 0;
+namespace {
+
+// One line-aligned chunk of an edge list, parsed independently.
+struct ChunkParse {
+    std::vector<uint64_t> ids;  // two per edge, in file order
+    uint64_t lines = 0;         // lines in the chunk (blank and comment lines included)
+    uint64_t err_line = 0;      // 1-based line (within the chunk) of the first error; 0 = none
+    std::string err;            // its message without the "line N: " prefix
+};
+
+void parse_chunk(const char* p, const char* end, ChunkParse& r) {
+    r.ids.reserve(static_cast<size_t>(end - p) / 6);
     while (p < end) {
         const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
         const char* le = nl ? nl : end;
-        ++line_no;
+        ++r.lines;
         const char* q = p;
         while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
         if (q == le || *q == '%' || *q == '#') {
@@ -307,21 +330,67 @@ HostGraph parse_edge_list_text(const char* text, uint64_t len) {
         }
         const char* c = p;
         uint64_t a = 0, b = 0;
-        if (!get_u64(c, le, a) || !get_u64(c, le, b))
-            parse_error("line " + std::to_string(line_no) + ": expected two vertex ids");
+        if (!get_u64(c, le, a) || !get_u64(c, le, b)) {
+            r.err_line = r.lines;
+            r.err = "expected two vertex ids";
+            return;
+        }
         while (c < le && is_space(*c)) ++c;
         if (c < le) {
             const char* te = c;
             while (te < le && !is_space(*te)) ++te;
-            parse_error("line " + std::to_string(line_no) + ": trailing token '" + std::string(c, te) + "'");
+            r.err_line = r.lines;
+            r.err = "trailing token '" + std::string(c, te) + "'";
+            return;
         }
-        if (a > 0xFFFFFFFFull || b > 0xFFFFFFFFull)
-            parse_error("line " + std::to_string(line_no) + ": vertex id exceeds 2^32-1");
-        const uint32_t da = in(a);  // interning order fixes the dense numbering
-        const uint32_t db = in(b);
-        edges.push_back(da);
-        edges.push_back(db);
+        if (a > 0xFFFFFFFFull || b > 0xFFFFFFFFull) {
+            r.err_line = r.lines;
+            r.err = "vertex id exceeds 2^32-1";
+            return;
+        }
+        r.ids.push_back(a);
+        r.ids.push_back(b);
         p = nl ? nl + 1 : end;
+    }
+}
+
+}  // namespace
+
+// graph.hpp:93-131. Line-aligned chunks are parsed on all host threads; the
+// first error in file order is reported with its global line number, and ids
+// are interned in file order afterwards (first appearance fixes the dense
+// numbering), so results and messages equal a sequential parse.
+HostGraph parse_edge_list_text(const char* text, uint64_t len) {
+    unsigned T = host_threads();
+    if (len < (uint64_t{4} << 20)) T = 1;
+    std::vector<uint64_t> cut(T + 1, len);
+    cut[0] = 0;
+    for (unsigned t = 1; t < T; ++t) {
+        uint64_t pos = std::max(cut[t - 1], len * t / T);
+        const char* nl = pos < len ? static_cast<const char*>(std::memchr(text + pos, '\n', len - pos)) : nullptr;
+        cut[t] = nl ? static_cast<uint64_t>(nl - text) + 1 : len;
+    }
+    std::vector<ChunkParse> parts(T);
+    if (T == 1) {
+        parse_chunk(text, text + len, parts[0]);
+    } else {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] { parse_chunk(text + cut[t], text + cut[t + 1], parts[t]); });
+        for (auto& x : th) x.join();
+    }
+    uint64_t lines_before = 0, total = 0;
+    for (const ChunkParse& r : parts) {
+        if (r.err_line) parse_error("line " + std::to_string(lines_before + r.err_line) + ": " + r.err);
+        lines_before += r.lines;
+        total += r.ids.size();
+    }
+    Interner in;
+    std::vector<uint32_t> edges(total);
+    uint64_t k = 0;
+    for (ChunkParse& r : parts) {
+        for (const uint64_t id : r.ids) edges[k++] = in(id);  // interning order fixes the dense numbering
+        std::vector<uint64_t>().swap(r.ids);
     }
     return finish(in, edges);
 }

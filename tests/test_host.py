@@ -54,6 +54,43 @@ def test_parse_errors(text, msg):
     assert str(e.value) == msg
 
 
+def _big_edge_list(lines: int, seed: int = 5) -> list[str]:
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, 40000, size=lines) * 7 + 3  # sparse ids: exercises the first-appearance remap
+    b = rng.integers(0, 40000, size=lines) * 7 + 3
+    out = [f"{x} {y}" for x, y in zip(a.tolist(), b.tolist())]
+    for i in range(0, lines, 997):
+        out[i] = "# comment " + out[i]  # comments and blank lines keep their line numbers
+    for i in range(5, lines, 1999):
+        out[i] = ""
+    return out
+
+
+def test_parse_parallel_chunks_match_oracle():
+    """Texts over 4 MB are parsed in line-aligned chunks on every host thread;
+    the CSR, the id remap and the error line numbers equal a sequential parse."""
+    lines = _big_edge_list(400_000)
+    text = "\n".join(lines) + "\n"
+    assert len(text) > (4 << 20)
+    p = adsamp.parse_edge_list(text)
+    o = oracle.parse_text(text)
+    np.testing.assert_array_equal(p.graph.offsets(), o.offsets)
+    np.testing.assert_array_equal(p.graph.neighbor_list(), o.nbrs)
+    np.testing.assert_array_equal(p.original_ids, o.original_ids)
+    for bad_line, bad in [(350_001, "12 x"), (123_457, "1 2 3"), (399_990, "5 99999999999")]:
+        broken = list(lines)
+        broken[bad_line - 1] = bad
+        later = bad_line + 20  # a second, later error must not win
+        if later <= len(broken):
+            broken[later - 1] = "only_one"
+        with pytest.raises(ParseError) as e:
+            adsamp.parse_edge_list("\n".join(broken))
+        with pytest.raises(Exception) as eo:
+            oracle.parse_text("\n".join(broken))
+        assert str(e.value).startswith(f"line {bad_line}: "), str(e.value)
+        assert str(e.value) == str(eo.value)
+
+
 def test_parse_file_and_pairs_agree(tmp_path):
     for name in ["er100", "cube", "two_components"]:
         pairs = SMALL_GRAPHS[name]().reshape(-1)
