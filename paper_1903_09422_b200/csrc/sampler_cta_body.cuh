@@ -33,7 +33,8 @@ struct Shared {
     uint32_t recorded, last_d;        // thread 0: increments recorded / last distance (fused audit)
     uint32_t lvl_cnt[3];              // per BFS level (slot = level % 3): vertices claimed,
     uint32_t lvl_deg[3];              //   their adjacency total (< 2^32: u32 offsets),
-    uint32_t lvl_ins[3];              //   hash reservations (shared-memory store)
+    uint32_t lvl_ins[3];              //   hash reservations (shared-memory store),
+    uint32_t lvl_met[3];              //   whether the frontiers met (any thread sets it)
     uint32_t s_cnt, t_cnt;            // queue fill: s-side from 0 up, t-side from the top down
     uint32_t overflow;
     uint32_t tlev_small[kSmemLevels]; // t-level boundaries (shared-memory store)
@@ -468,7 +469,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     // So a level needs no barrier of its own before it starts claiming.
     S.set_level(&sh.lvl_ins[2], 0);
     if (C.tid == 0) {
-        for (int i = 0; i < 3; ++i) sh.lvl_cnt[i] = sh.lvl_deg[i] = sh.lvl_ins[i] = 0;
+        for (int i = 0; i < 3; ++i) sh.lvl_cnt[i] = sh.lvl_deg[i] = sh.lvl_ins[i] = sh.lvl_met[i] = 0;
         bool ins;
         uint32_t m;
         const uint32_t ss = S.claim(s, 0u, ins, m);
@@ -489,13 +490,12 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
     for (;;) {
         const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
-        if (C.tid == 0) sh.lvl_cnt[nxt] = sh.lvl_deg[nxt] = sh.lvl_ins[nxt] = 0;
+        if (C.tid == 0) sh.lvl_cnt[nxt] = sh.lvl_deg[nxt] = sh.lvl_ins[nxt] = sh.lvl_met[nxt] = 0;
         S.set_level(&sh.lvl_ins[cur], used);
         if (deg_s <= deg_t && S.room_for(deg_s)) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
-            bool met = false;
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -511,12 +511,12 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           } else if (m_is_t(m) && m_dist(m) == b) {
                               S.add_sigma(sl, su);
                               if (!(m & kMetaDag)) S.set_dag(sl);
-                              met = true;
+                              sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           } else if (Store::kSigmaPreZeroed && !m_is_t(m) && m_dist(m) == a + 1) {
                               S.add_sigma(sl, su);
                           }
                       });
-            met = __syncthreads_or(met);
+            const bool met = sh.lvl_met[cur] != 0;  // for_edges ended with a barrier
             const uint32_t added = sh.lvl_cnt[cur];
             if (met) {
                 if (C.tid == 0) sh.s_cnt = s_hi + added;  // the table clear walks the queue
@@ -540,7 +540,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
-            bool met = false;
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -556,10 +555,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           } else if (!m_is_t(m) && m_dist(m) == a) {
                               S.add_sigma(su_slot, S.sigma(sl));
                               S.set_dag(su_slot);
-                              met = true;
+                              sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           }
                       });
-            met = __syncthreads_or(met);
+            const bool met = sh.lvl_met[cur] != 0;
             const uint32_t added = sh.lvl_cnt[cur];
             if (met) {
                 if (C.tid == 0) sh.t_cnt = t_hi + added;
@@ -579,7 +578,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
-            bool met = false;
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -588,10 +586,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (sl != kNone && m_is_t(m) && m_dist(m) == b) {
                               S.add_sigma(sl, su);
                               if (!(m & kMetaDag)) S.set_dag(sl);
-                              met = true;
+                              sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           }
                       });
-            if (__syncthreads_or(met)) return {a, b, 0};
+            if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
@@ -630,7 +628,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else {
             // ---- t-side level b: probe for the s-ball
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
-            bool met = false;
             for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
@@ -639,10 +636,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                           if (sl != kNone && !m_is_t(m) && m_dist(m) == a) {
                               S.add_sigma(su_slot, S.sigma(sl));
                               S.set_dag(su_slot);
-                              met = true;
+                              sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           }
                       });
-            if (__syncthreads_or(met)) return {a, b, 0};
+            if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
