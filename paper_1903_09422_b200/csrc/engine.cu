@@ -174,11 +174,13 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     // small-world graphs (C2/C3). ADSB_SAMPLER overrides.
     SamplerKind kind = n <= (1u << 16) ? SamplerKind::kWarp : SamplerKind::kBlock;
     if (std::getenv("ADSB_SAMPLER")) kind = sampler_kind();
-    uint32_t hash_cap = 2048;
+    // 2 304 entries (1 152 insertions): the most that keeps 4 blocks per SM and,
+    // measured over 2 048-3 072, the fastest on C3/C5 (fewer global fallbacks)
+    uint32_t hash_cap = 2304;
     if (const char* e = std::getenv("ADSB_HASH_CAP")) hash_cap = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     uint32_t block_threads = 256;
     if (const char* e = std::getenv("ADSB_BLOCK")) block_threads = std::strtoul(e, nullptr, 10) == 128 ? 128 : 256;
-    if (hash_cap < 64 || (hash_cap & (hash_cap - 1))) invalid("ADSB_HASH_CAP must be a power of two >= 64");
+    if (hash_cap < 64 || hash_cap % 64) invalid("ADSB_HASH_CAP must be a multiple of 64");
     const int k = kind == SamplerKind::kWarp ? 0 : 1;
     DeviceRuntime& rt = *ctx.rt;
     rt.active = k;

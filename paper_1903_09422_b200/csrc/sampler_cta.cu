@@ -179,6 +179,8 @@ void sampler_phase_report() {
                  "kernel per block %.3g, samples %llu, levels/sample %.2f, edge passes/sample %.2f\n",
                  h[0] / samples, h[1] / samples, h[2] / samples, h[3] / samples, static_cast<double>(h[4]),
                  h[7], h[5] / samples, h[6] / samples);
+    std::fprintf(stderr, "[adsb]   sample cycles (thread 0): fallback samples %.3g total, others %.3g total\n",
+                 static_cast<double>(h[14]), static_cast<double>(h[15]));
     std::fprintf(stderr,
                  "[adsb]   for_edges per chunk: prep %.0f, edge loop (thread 0) %.0f, end barrier wait %.0f | "
                  "edges/chunk %.1f, chunks/sample %.2f, level degree passes %.0f per sample\n",

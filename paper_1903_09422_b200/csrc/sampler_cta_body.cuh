@@ -63,8 +63,7 @@ struct SmemStore {
     unsigned long long* sig;
     uint32_t* qv;      // queue: vertex ids
     uint32_t* tlev;
-    uint32_t mask;
-    uint32_t shift;
+    uint32_t cap;      // table entries (any size: slots come from a multiply-high)
     uint32_t qcap;
     uint32_t limit;    // max insertions (<= capacity/2 keeps probing short and finite)
     uint32_t level_cap;
@@ -77,17 +76,17 @@ struct SmemStore {
         ins_base = base;
     }
     __device__ uint32_t home(uint32_t v) const {
-        return ((v * 0x9E3779B1u) >> shift) & mask;  // Fibonacci hashing on 32 bits
+        return __umulhi(v * 0x9E3779B1u, cap);  // Fibonacci hash scaled onto [0, cap)
     }
     __device__ void clear_all(uint32_t tid) {
-        for (uint32_t i = tid; i <= mask; i += kBT) {
+        for (uint32_t i = tid; i < cap; i += kBT) {
             km[i] = ~0ull;
             sig[i] = 0ull;
         }
     }
     __device__ void begin(uint32_t tid) {
 #ifdef ADSB_DEBUG_CHECKS
-        for (uint32_t i = tid; i <= mask; i += kBT)
+        for (uint32_t i = tid; i < cap; i += kBT)
             ADSB_DCHECK(km[i] == ~0ull && sig[i] == 0ull, "hash table not clean at sample start");
 #endif
     }
@@ -127,7 +126,7 @@ struct SmemStore {
                 return h;
             }
             if (k == kEmptyKey) return kNone;
-            h = (h + 1) & mask;
+            h = h + 1 < cap ? h + 1 : 0u;
         }
     }
     // returns the slot (kNone on overflow); inserted tells whether this call
@@ -166,7 +165,7 @@ struct SmemStore {
                     return h;
                 }
             }
-            h = (h + 1) & mask;
+            h = h + 1 < cap ? h + 1 : 0u;
         }
     }
     static constexpr bool kSigmaPreZeroed = true;  // claim and sigma accumulation share one pass
@@ -970,8 +969,7 @@ __device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Sha
     sm.qcap = H / 2;
     sm.qv = reinterpret_cast<uint32_t*>(adsb_dyn + 2 * H);
     sm.tlev = sh.tlev_small;
-    sm.mask = H - 1;
-    sm.shift = 32 - (31 - __clz(H));
+    sm.cap = H;
     sm.limit = H / 2;
     sm.level_cap = kSmemLevels;
     sm.sh = &sh;
@@ -1028,6 +1026,7 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
     if (t >= s) ++t;
     if (C.tid == 0) C.sh->last_d = 0xFFFF;
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
+    ADSB_PHASE_MARK(os0);
     int rc = 1;
     if constexpr (!kGlobalOnly) {
         if (p.use_smem) {
@@ -1035,6 +1034,8 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
         }
     }
+    const bool fell_back = rc == 1;
+    (void)fell_back;
     if (rc == 1) {
         uint32_t region = blockIdx.x, tag;
         if constexpr (kGlobalOnly) {
@@ -1058,6 +1059,8 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
         }
     }
     if (rc != 0 && C.tid == 0) C.sh->n_errors += 1;
+    ADSB_PHASE_MARK(os1);
+    ADSB_PHASE_ADD(fell_back ? 14 : 15, os1 - os0);
 }
 
 __device__ __forceinline__ unsigned long long vload(const unsigned long long* a) {
