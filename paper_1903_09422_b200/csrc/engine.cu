@@ -71,6 +71,8 @@ bool converged_at_max(uint64_t max_count, uint64_t tau, uint64_t omega, double e
 namespace {
 
 constexpr uint32_t kNoStop = 0xFFFFFFFFu;
+// the shared-memory table stores vertex + 1 in 24 bits (sampler_cta_body.cuh SmemStore)
+constexpr uint32_t kSmemMaxN = (1u << 24) - 1;
 // word offsets into DeviceContext::pinned (words 0..15 belong to the BFS level counts)
 constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
               kPinAdapt = 72, kPinCtl = 80, kPinCursor = 96;  // kPinCtl: 9 words; kPinCursor: 2 words
@@ -174,9 +176,9 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     // small-world graphs (C2/C3). ADSB_SAMPLER overrides.
     SamplerKind kind = n <= (1u << 16) ? SamplerKind::kWarp : SamplerKind::kBlock;
     if (std::getenv("ADSB_SAMPLER")) kind = sampler_kind();
-    // 2 304 entries (1 152 insertions): the most that keeps 4 blocks per SM and,
-    // measured over 2 048-3 072, the fastest on C3/C5 (fewer global fallbacks)
-    uint32_t hash_cap = 2304;
+    // 2 944 entries of 14 B (1 472 insertions): the shared memory of the former
+    // 2 304 x 18 B table, 4 blocks per SM (profiles/r01_hash_cap_sweep.txt)
+    uint32_t hash_cap = 2944;
     if (const char* e = std::getenv("ADSB_HASH_CAP")) hash_cap = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     uint32_t block_threads = 256;
     if (const char* e = std::getenv("ADSB_BLOCK")) block_threads = std::strtoul(e, nullptr, 10) == 128 ? 128 : 256;
@@ -363,7 +365,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (ctx.use_smem < 0) {
         // Deep graphs (grid: D_ub 8182) need far more t-levels than the table
         // tracks and far larger balls than it holds: go global-only at once.
-        ctx.use_smem = std::getenv("ADSB_NO_SMEM") || out.diameter_bound > 128 ? 0 : 1;
+        ctx.use_smem = std::getenv("ADSB_NO_SMEM") || out.diameter_bound > 128 || n >= kSmemMaxN ? 0 : 1;
     }
     out.preprocess_seconds = pre.seconds();
     if (trace_enabled())
@@ -883,7 +885,7 @@ void sample_frames(DeviceContext& ctx, uint64_t seed, uint64_t spf, uint64_t fir
     device_components(ctx);
     const uint64_t dub = device_diameter_bound(ctx);
     ensure_arena(ctx, static_cast<uint32_t>(std::min<uint64_t>(dub + 3, ctx.graph.n + 2)));
-    if (ctx.use_smem < 0) ctx.use_smem = std::getenv("ADSB_NO_SMEM") || dub > 128 ? 0 : 1;
+    if (ctx.use_smem < 0) ctx.use_smem = std::getenv("ADSB_NO_SMEM") || dub > 128 || ctx.graph.n >= kSmemMaxN ? 0 : 1;
     unsigned long long* events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, 1 << 16);
     unsigned long long* scal = ctx.rt->pool.get<unsigned long long>(Scratch::kScal, 4);
     unsigned long long* stats = ctx.rt->pool.get<unsigned long long>(Scratch::kStats, kStatCount);

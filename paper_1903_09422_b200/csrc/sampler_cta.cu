@@ -92,7 +92,7 @@ constexpr int kBT = 256;
 }  // namespace bt256
 
 size_t sampler_cta_smem_bytes(uint32_t hash_cap) {
-    return static_cast<size_t>(hash_cap) * 16 + static_cast<size_t>(hash_cap / 2) * 4;  // km, sigma, queue
+    return static_cast<size_t>(hash_cap) * 12 + static_cast<size_t>(hash_cap / 2) * 4;  // sigma, key|meta, queue
 }
 
 namespace {

@@ -59,8 +59,13 @@ struct Shared {
 // so concurrent claimers and adders never race on initialisation).
 struct SmemStore {
     static constexpr uint32_t kLoadBatch = ADSB_LOAD_BATCH;
-    unsigned long long* km;
+    // Entry = one u32: (vertex + 1) << 8 | meta8 (bit 7 t-side, bit 6 DAG,
+    // bits 0-5 distance); 0 = empty. Needs n < 2^24 - 1 and distances <= 63
+    // (larger graphs use the global store; a deeper level overflows to it).
+    // Sigma sits in its own u64 array: 12 B per entry plus 2 B of queue.
+    static constexpr uint32_t kMaxDist = 62;  // levels a+1, b+1 stay <= 63
     unsigned long long* sig;
+    uint32_t* km;
     uint32_t* qv;      // queue: vertex ids
     uint32_t* tlev;
     uint32_t cap;      // table entries (any size: slots come from a multiply-high)
@@ -71,6 +76,12 @@ struct SmemStore {
     uint32_t* ins_ctr;  // this level's reservation counter (Shared::lvl_ins slot)
     uint32_t ins_base;  // reservations made before this level (same in every thread)
 
+    static __device__ __forceinline__ uint32_t decode(uint32_t w) {
+        return ((w & 0x80u) ? kMetaT : 0u) | ((w & 0x40u) ? kMetaDag : 0u) | (w & 0x3Fu);
+    }
+    static __device__ __forceinline__ uint32_t encode(uint32_t v, uint32_t meta) {
+        return ((v + 1u) << 8) | ((meta & kMetaT) ? 0x80u : 0u) | (m_dist(meta) & 0x3Fu);
+    }
     __device__ void set_level(uint32_t* ctr, uint32_t base) {
         ins_ctr = ctr;
         ins_base = base;
@@ -80,14 +91,14 @@ struct SmemStore {
     }
     __device__ void clear_all(uint32_t tid) {
         for (uint32_t i = tid; i < cap; i += kBT) {
-            km[i] = ~0ull;
+            km[i] = 0u;
             sig[i] = 0ull;
         }
     }
     __device__ void begin(uint32_t tid) {
 #ifdef ADSB_DEBUG_CHECKS
         for (uint32_t i = tid; i < cap; i += kBT)
-            ADSB_DCHECK(km[i] == ~0ull && sig[i] == 0ull, "hash table not clean at sample start");
+            ADSB_DCHECK(km[i] == 0u && sig[i] == 0ull, "hash table not clean at sample start");
 #endif
     }
     // Reset exactly the slots this sample inserted (the queue lists them) so
@@ -111,21 +122,21 @@ struct SmemStore {
             __syncthreads();
             for (uint32_t i = C.tid; i < ns + nt; i += kBT) {
                 const uint32_t h = qv[i < ns ? i : tpos(i - ns)];
-                if (h != kNone) km[h] = ~0ull;
+                if (h != kNone) km[h] = 0u;
             }
         }
         __syncthreads();
     }
     __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
+        const uint32_t key = v + 1u;
         uint32_t h = home(v);
         for (;;) {
-            const unsigned long long x = km[h];
-            const uint32_t k = static_cast<uint32_t>(x >> 32);
-            if (k == v) {
-                meta = static_cast<uint32_t>(x);
+            const uint32_t w = km[h];
+            if ((w >> 8) == key) {
+                meta = decode(w);
                 return h;
             }
-            if (k == kEmptyKey) return kNone;
+            if (w == 0u) return kNone;
             h = h + 1 < cap ? h + 1 : 0u;
         }
     }
@@ -136,16 +147,16 @@ struct SmemStore {
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
         meta = ~0u;  // on overflow: matches no side/level test
+        const uint32_t key = v + 1u;
         uint32_t h = home(v);
         bool reserved = !kReserve;
         for (;;) {
-            unsigned long long x = km[h];
-            uint32_t k = static_cast<uint32_t>(x >> 32);
-            if (k == v) {
-                meta = static_cast<uint32_t>(x);
+            const uint32_t w = km[h];
+            if ((w >> 8) == key) {
+                meta = decode(w);
                 return h;
             }
-            if (k == kEmptyKey) {
+            if (w == 0u) {
                 if (!reserved) {
                     if (atomicAdd(ins_ctr, 1u) + ins_base >= limit) {
                         sh->overflow = 1;
@@ -153,15 +164,14 @@ struct SmemStore {
                     }
                     reserved = true;
                 }
-                const unsigned long long want = (static_cast<unsigned long long>(v) << 32) | new_meta;
-                const unsigned long long prev = atomicCAS(&km[h], x, want);
-                if (prev == x) {
+                const uint32_t prev = atomicCAS(&km[h], 0u, encode(v, new_meta));
+                if (prev == 0u) {
                     inserted = true;
                     meta = new_meta;
                     return h;
                 }
-                if (static_cast<uint32_t>(prev >> 32) == v) {
-                    meta = static_cast<uint32_t>(prev);
+                if ((prev >> 8) == key) {
+                    meta = decode(prev);
                     return h;
                 }
             }
@@ -185,9 +195,7 @@ struct SmemStore {
         }
         if (xh | carry) atomicAdd(w + 1, xh + carry);
     }
-    // the meta half (low word) of key << 32 | meta; no claim CASes a slot that
-    // already holds a key, so the 32-bit OR never overlaps a 64-bit CAS
-    __device__ void set_dag(uint32_t slot) { atomicOr(reinterpret_cast<uint32_t*>(&km[slot]), kMetaDag); }
+    __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], 0x40u); }
     __device__ unsigned long long sigma(uint32_t slot) const { return sig[slot]; }
     __device__ bool queue_ok(uint32_t s_cnt, uint32_t t_cnt) const { return s_cnt + t_cnt <= qcap; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
@@ -204,6 +212,7 @@ struct SmemStore {
 template <uint32_t kU>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
+    static constexpr uint32_t kMaxDist = kMetaDist - 1;
     unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* tlev;
@@ -488,6 +497,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     uint32_t used = sh.lvl_ins[2];  // reservations so far (s and t)
     unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
     for (;;) {
+        if (a >= Store::kMaxDist || b >= Store::kMaxDist) return {a, b, 1};  // deeper than the store encodes
         const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
         if (C.tid == 0) sh.lvl_cnt[nxt] = sh.lvl_deg[nxt] = sh.lvl_ins[nxt] = sh.lvl_met[nxt] = 0;
         S.set_level(&sh.lvl_ins[cur], used);
@@ -964,10 +974,10 @@ extern __shared__ unsigned long long adsb_dyn[];
 __device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Shared& sh) {
     SmemStore sm;
     const uint32_t H = p.hash_cap;
-    sm.km = adsb_dyn;
-    sm.sig = adsb_dyn + H;
+    sm.sig = adsb_dyn;                                     // H x u64
+    sm.km = reinterpret_cast<uint32_t*>(adsb_dyn + H);     // H x u32
     sm.qcap = H / 2;
-    sm.qv = reinterpret_cast<uint32_t*>(adsb_dyn + 2 * H);
+    sm.qv = sm.km + H;                                     // H/2 x u32
     sm.tlev = sh.tlev_small;
     sm.cap = H;
     sm.limit = H / 2;
