@@ -808,12 +808,15 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             __syncthreads();
             if (!found) return false;
         }
+        // the next round's neighbour id is loaded one round ahead, so its
+        // latency overlaps this round's barriers (hub steps take many rounds)
+        uint32_t q_next = !found && beg + C.tid < end ? C.nbrs[beg + C.tid] : 0u;
         for (uint32_t base = beg; !found && base < end; base += kBT) {
             const uint32_t i = base + C.tid;
-            uint32_t q = 0, m = 0;
+            uint32_t q = q_next, m = 0;
             unsigned long long val = 0;
+            if (i + kBT < end) q_next = C.nbrs[i + kBT];
             if (i < end) {
-                q = C.nbrs[i];
                 const uint32_t sl = S.find(q, m);
                 if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag)))
                     val = S.sigma(sl);
