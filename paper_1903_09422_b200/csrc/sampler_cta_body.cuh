@@ -389,6 +389,10 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                         have = true;
                     }
                     vv[k] = C.nbrs[o_base + e];
+                    // pull this thread's next adjacency id into L1 while the
+                    // body runs (same row: the common case inside hub lists)
+                    if (k + 1 == kBatch && e + kBT < o_end)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(C.nbrs + o_base + e + kBT));
                     owners |= ow << (8 * k);
                     cnt = k + 1;
                 }
@@ -1027,8 +1031,10 @@ __device__ uint32_t acquire_region(const SamplerParams& p) {
 
 __device__ void release_region(const SamplerParams& p, uint32_t region, uint32_t tag) {
     p.slot_tag[region] = tag;
-    __threadfence();
-    atomicAnd(p.slot_busy + region / 32, ~(1u << (region & 31)));
+    // release: the tag is visible before the region is free (no L1 invalidation)
+    asm volatile("red.release.gpu.global.and.b32 [%0], %1;" ::"l"(p.slot_busy + region / 32),
+                 "r"(~(1u << (region & 31)))
+                 : "memory");
 }
 
 // gtag: the global-only kernel's generation tag for its own region (block-uniform).
@@ -1256,8 +1262,16 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
             if (C.tid == 0) {
                 if (p.audit && item < p.max_epochs * p.epoch_b)
                     p.audit[item] = (sh.recorded - rec0) | (sh.last_d << 16);
-                __threadfence();  // this sample's counts before its completion
-                sh.done_old = atomicAdd(p.ctl + kCtlDone + k, 1ull);
+                // release: this sample's counts and list entries become visible
+                // before its completion does. A release atomic, not
+                // __threadfence(): the full fence also invalidates the SM's L1
+                // (CCTL.IVALL) after every sample, losing adjacency reuse.
+                unsigned long long old;
+                asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;"
+                             : "=l"(old)
+                             : "l"(p.ctl + kCtlDone + k), "l"(1ull)
+                             : "memory");
+                sh.done_old = old;
                 sh.pending = 1;
             }
         }
