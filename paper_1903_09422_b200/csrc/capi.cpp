@@ -5,6 +5,7 @@
 // codes via adsb::guard (common.hpp).
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -304,11 +305,15 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
         Locked L = locked_context(g, device);
         EngineOutput r = adsb::estimate_bc(L.ctx, epsilon, delta, opt);
         const uint32_t n = g->host.n;
-        for (uint32_t v = 0; v < n; ++v) {
-            if (counts) counts[v] = r.counts[v];
-            if (scores)  // kadabra.hpp:334-337
-                scores[v] = r.tau == 0 ? 0.0 : static_cast<double>(r.counts[v]) / static_cast<double>(r.tau);
+        // r.counts points into the runtime's pinned buffer: copied out while the
+        // runtime lock (L) is still held
+        if (counts) {
+            if (r.counts) std::copy(r.counts, r.counts + n, counts);
+            else std::fill(counts, counts + n, uint64_t{0});
         }
+        if (scores)  // kadabra.hpp:334-337
+            for (uint32_t v = 0; v < n; ++v)
+                scores[v] = r.tau == 0 || !r.counts ? 0.0 : static_cast<double>(r.counts[v]) / static_cast<double>(r.tau);
         if (stats) {
             stats->tau = r.tau;
             stats->check_cycles = r.check_cycles;

@@ -342,8 +342,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (!(eps > 0.0 && eps < 1.0)) invalid("epsilon must lie in (0,1)");
     ADSB_CUDA(cudaSetDevice(ctx.device));
     if (n == 1) {  // kadabra.hpp:314-317
-        out.counts.assign(1, 0);
-        return out;
+        return out;  // counts == nullptr: the single vertex scores 0
     }
     const int world = opt.comm ? opt.comm->nranks : 1;
     const int rank = opt.comm ? opt.comm->rank : 0;
@@ -706,6 +705,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             p.audit = ctx.rt->pool.get<uint32_t>(Scratch::kAudit, (B + 1) * max_epochs);
             ADSB_CUDA(cudaMemsetAsync(p.audit, 0, (B + 1) * max_epochs * sizeof(uint32_t), s1));
         }
+        const double t_launch = ads.seconds();
         ADSB_CUDA(cudaEventRecord(e0, s1));
         launch_sampler_fused(p, s1);
         ADSB_CUDA(cudaEventRecord(e1, s1));
@@ -734,9 +734,9 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             }
         }
         if (trace_enabled())
-            std::fprintf(stderr, "[adsb] fused epochs: B %llu stop epoch %llu drawn %llu t=%.3f ms\n",
+            std::fprintf(stderr, "[adsb] fused epochs: B %llu stop epoch %llu drawn %llu launch at %.3f ms, t=%.3f ms\n",
                          static_cast<unsigned long long>(B), static_cast<unsigned long long>(stop),
-                         static_cast<unsigned long long>(out.total_samples), 1e3 * ads.seconds());
+                         static_cast<unsigned long long>(out.total_samples), 1e3 * t_launch, 1e3 * ads.seconds());
     } else {
         // ---- cumulative epoch pipeline
         uint64_t B = opt.epoch_samples;
@@ -852,7 +852,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (st_host[kStatErrors] != 0)
         fail(ADSB_ERR_LOGIC, "sampler reported " + std::to_string(st_host[kStatErrors]) +
                                  " inconsistent traversals (all predecessor counts wrapped to 0?)");
-    out.counts.assign(host32, host32 + n);
+    out.counts = host32;
     out.edges_scanned = st_host[kStatEdges];
     out.vertices_expanded = st_host[kStatVertices];
     out.rebuild_edges = st_host[kStatRebuildEdges];
@@ -869,7 +869,11 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             out.reason = ADSB_REASON_EPS_CONVERGED;
     }
     out.ads_seconds = ads.seconds();
-    if (trace_enabled()) sampler_phase_report();
+    if (trace_enabled()) {
+        std::fprintf(stderr, "[adsb] results at %.3f ms (pre %.3f ms)\n", 1e3 * out.ads_seconds,
+                     1e3 * out.preprocess_seconds);
+        sampler_phase_report();
+    }
     return out;
 }
 

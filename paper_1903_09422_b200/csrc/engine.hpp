@@ -22,7 +22,9 @@ struct EngineOptions {
 };
 
 struct EngineOutput {
-    std::vector<uint64_t> counts;  // RunResult::data
+    // RunResult::data: the pinned download buffer of the device runtime, valid
+    // while the caller holds the runtime lock (capi copies it out); nullptr = all 0
+    const uint32_t* counts = nullptr;
     uint64_t tau = 0, check_cycles = 0, stop_epoch = 0, total_samples = 0;
     uint64_t omega = 0, diameter_bound = 0;
     int32_t reason = ADSB_REASON_EPS_CONVERGED;

