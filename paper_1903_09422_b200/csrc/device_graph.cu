@@ -13,6 +13,7 @@
 // D_ub: one multi-source, level-synchronous BFS from every component's
 // max-degree vertex (lowest id on ties); the deepest level is the largest
 // eccentricity, D_ub = 2 * that.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -165,11 +166,55 @@ __global__ void init_dist(uint32_t* dist, uint32_t n) {
         dist[v] = kInf;
 }
 
-// K6: one level of a (multi-source) BFS; warp per frontier vertex.
+// Next free position of a counter for the converged lanes of a warp (one
+// atomic per group).
+__device__ __forceinline__ uint32_t warp_agg_inc(uint32_t* ctr) {
+    namespace cg = cooperative_groups;
+    const cg::coalesced_group g = cg::coalesced_threads();
+    uint32_t base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(ctr, g.size());
+    return g.shfl(base, 0) + g.thread_rank();
+}
+
+// K6: one level of a (multi-source) BFS, direction chosen on the device from
+// the frontier size (every level of a chunk is launched without a host check):
+// * large frontier (> n/24): bottom-up. Every unvisited vertex looks for a
+//   neighbour on this level and stops at the first; only its own thread
+//   writes dist[v]. This covers the few huge middle levels of small-world graphs.
+// * frontier smaller than the grid: one block per frontier vertex (a hub
+//   source would otherwise be walked by a single warp);
+// * otherwise one warp per frontier vertex.
+// The depth and dist values equal any level-synchronous BFS's.
 __global__ void bfs_level(const uint32_t* __restrict__ off, const uint32_t* __restrict__ nbrs,
                           uint32_t* dist, const uint32_t* __restrict__ fin, const uint32_t* cnt_in,
-                          uint32_t* fout, uint32_t* cnt_out, uint32_t level) {
+                          uint32_t* fout, uint32_t* cnt_out, uint32_t level, uint32_t n) {
     const uint32_t count = *cnt_in;
+    if (count == 0) return;
+    if (count > n / 24) {
+        for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+            if (dist[v] != kInf) continue;
+            const uint32_t b = off[v], e = off[v + 1];
+            for (uint32_t j = b; j < e; ++j) {
+                if (__ldcg(dist + nbrs[j]) == level) {
+                    dist[v] = level + 1;
+                    fout[warp_agg_inc(cnt_out)] = v;
+                    break;
+                }
+            }
+        }
+        return;
+    }
+    if (count <= gridDim.x) {
+        for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+            const uint32_t u = fin[i];
+            const uint32_t b = off[u], e = off[u + 1];
+            for (uint32_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+                const uint32_t w = nbrs[j];
+                if (dist[w] == kInf && atomicCAS(&dist[w], kInf, level + 1) == kInf) fout[warp_agg_inc(cnt_out)] = w;
+            }
+        }
+        return;
+    }
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -178,8 +223,7 @@ __global__ void bfs_level(const uint32_t* __restrict__ off, const uint32_t* __re
         const uint32_t b = off[u], e = off[u + 1];
         for (uint32_t j = b + lane; j < e; j += 32) {
             const uint32_t w = nbrs[j];
-            if (dist[w] == kInf && atomicCAS(&dist[w], kInf, level + 1) == kInf)
-                fout[atomicAdd(cnt_out, 1u)] = w;
+            if (dist[w] == kInf && atomicCAS(&dist[w], kInf, level + 1) == kInf) fout[warp_agg_inc(cnt_out)] = w;
         }
     }
 }
@@ -340,7 +384,7 @@ static uint64_t bfs_depth(DeviceContext& ctx, uint32_t* dist, uint32_t* fa, uint
             uint32_t* fin = (L & 1) ? fb : fa;
             uint32_t* fout = (L & 1) ? fa : fb;
             bfs_level<<<grid, 256, 0, s>>>(ctx.graph.offsets.ptr, ctx.graph.nbrs.ptr, dist, fin, counts + L, fout,
-                                           counts + L + 1, L);
+                                           counts + L + 1, L, n);
         }
         const uint32_t avail = std::min<uint32_t>(kChunk, n - level);
         ADSB_CUDA(cudaMemcpyAsync(host, counts + level + 1, avail * sizeof(uint32_t),

@@ -47,7 +47,7 @@ struct HostBlockCache {
     std::map<size_t, std::vector<void*>> free;  // size class (power of two) -> blocks
     size_t cached = 0;
     int pinned = -1;  // -1 unknown, 0 malloc, 1 cudaHostAlloc
-    static constexpr size_t kCap = size_t{2} << 30;
+    static constexpr size_t kCap = size_t{8} << 30;  // page-locked bytes kept for reuse
 };
 
 HostBlockCache& host_cache() {
@@ -55,10 +55,13 @@ HostBlockCache& host_cache() {
     return *c;
 }
 
+// Size classes: multiples of 1/8 of the enclosing power of two (at most 12.5%
+// slack: a 2.1 GB adjacency array must not round up to 4 GB of pinned memory).
 size_t size_class(size_t bytes) {
-    size_t c = kHostBlockMin;
-    while (c < bytes) c <<= 1;
-    return c;
+    size_t p = kHostBlockMin;
+    while (p < bytes) p <<= 1;
+    const size_t step = std::max(kHostBlockMin, p / 8);
+    return (bytes + step - 1) / step * step;
 }
 
 }  // namespace
