@@ -74,7 +74,7 @@ constexpr uint32_t kNoStop = 0xFFFFFFFFu;
 // the shared-memory table stores vertex + 1 in 24 bits (sampler_cta_body.cuh SmemStore)
 constexpr uint32_t kSmemMaxN = (1u << 24) - 1;
 // word offsets into DeviceContext::pinned (words 0..15 belong to the BFS level counts)
-constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
+constexpr int kPinUsed = 48, kPinStop = 49, kPinEmax = 50, kPinMax = 51, kPinFlags = 52, kPinStat0 = 56, kPinStats = 64,
               kPinAdapt = 72, kPinCtl = 80, kPinCursor = 96;  // kPinCtl: 9 words; kPinCursor: 2 words
 static_assert(kStatCount <= 8, "pinned staging layout");
 
@@ -386,6 +386,9 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     }
     cudaEvent_t e0 = ctx.rt->ev_a, e1 = ctx.rt->ev_b;
     Launches L;
+    const uint32_t* max_dev32 = nullptr;  // device copy of max_v counts[v] when a branch keeps one
+    bool max_known = false;
+    uint64_t max_host = 0;
     // work units that keep every team busy: warps are many and light, blocks few and heavy
     const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).blocks;
 
@@ -567,6 +570,8 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         bool stopped = false;
         uint32_t stop_local = kNoStop;
         uint64_t cur_max = 0;  // largest count after the frames folded so far
+        uint64_t growth = 3;   // batch cap: growth x the frames done (ADSB_DET_GROWTH; 3 beat 2 and 4 on C1/C3/C4)
+        if (const char* g = std::getenv("ADSB_DET_GROWTH")) growth = std::max<uint64_t>(2, std::strtoull(g, nullptr, 10));
         while (!stopped) {
             // Batch size: the predicted remaining frames (+5%), at least a few
             // frames per team; the first batch has no prediction yet.
@@ -574,10 +579,10 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             if (done > 0) {
                 const uint64_t tau_star = predict_stop_tau(cur_max, done * spf, out.omega, eps, log_inv);
                 const uint64_t need = (tau_star > done * spf ? (tau_star - done * spf + spf - 1) / spf : 1);
-                // never more than the doubling schedule: early max counts are
+                // at most `growth` x the frames done so far: early max counts are
                 // biased high, so the prediction overshoots then
                 F = std::min<uint64_t>(std::max<uint64_t>(need + need / 20 + 1, team_slots * world / 2),
-                                       std::max<uint64_t>(done, F));
+                                       std::max<uint64_t>((growth - 1) * done, F));
             }
             F = std::min<uint64_t>(F, frame_limit - done);
             F = std::min<uint64_t>(F, 1ull << 30);
@@ -664,6 +669,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             if (!stopped) done += F;
             else done += static_cast<uint64_t>(stop_local) + 1;
         }
+        max_dev32 = base_max;  // k_update_base folded the running max up to the stop frame
         out.total_samples = sampled_frames * spf;
         out.check_cycles = done;
         out.tau = done * spf;
@@ -722,6 +728,8 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         out.tau = (stop + 1) * B;
         out.check_cycles = stop + 1;
         out.stop_epoch = stop + 1;
+        max_host = ctl_h[kCtlMax];  // running max of the folded epochs (fold_chain)
+        max_known = true;
         ADSB_CUDA(cudaMemcpyAsync(ctl_h + 8, stats + kStatSamples, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
         ADSB_CUDA(cudaStreamSynchronize(s1));
         out.total_samples = ctl_h[8];
@@ -847,6 +855,8 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     ADSB_CUDA(cudaMemcpyAsync(host32, total, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
     unsigned long long* st_host = ctx.rt->pinned.ptr + kPinStats;
     ADSB_CUDA(cudaMemcpyAsync(st_host, stats, kStatCount * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
+    uint32_t* max_h32 = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinMax);
+    if (max_dev32) ADSB_CUDA(cudaMemcpyAsync(max_h32, max_dev32, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
     ADSB_CUDA(cudaStreamSynchronize(s1));
     ADSB_CUDA(cudaGetLastError());
     if (st_host[kStatErrors] != 0)
@@ -864,7 +874,10 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     if (out.reason != ADSB_REASON_CAPPED) {
         out.reason = ADSB_REASON_OMEGA_REACHED;
         uint64_t mx = 0;
-        for (uint32_t v = 0; v < n; ++v) mx = std::max<uint64_t>(mx, host32[v]);
+        if (max_dev32) mx = *max_h32;
+        else if (max_known) mx = max_host;
+        else
+            for (uint32_t v = 0; v < n; ++v) mx = std::max<uint64_t>(mx, host32[v]);
         if (out.tau >= 1 && converged_at_max(mx, out.tau, out.omega, eps, log_inv))
             out.reason = ADSB_REASON_EPS_CONVERGED;
     }
