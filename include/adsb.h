@@ -150,6 +150,13 @@ adsb_status adsb_sample_frames(const adsb_graph *g, int device, uint64_t seed, u
                                uint64_t first, uint64_t count, uint64_t *frame_offsets,
                                uint32_t *incs, uint64_t cap);
 
+/* ---- validation: exact BC on the device (Brandes, f64) ---------------------- */
+/* Exact betweenness of every vertex, normalised by n(n-1) like estimate_bc's
+ * scores: the check the reference makes against ApspOracle / Brandes
+ * (tests/test_util.hpp:164-206, tests/acceptance.cpp:60-101), on the GPU so
+ * that it reaches graphs of C2's size. device_ms (nullable) receives the
+ * kernel time. */
+adsb_status adsb_exact_bc(const adsb_graph *g, int device, double *bc /* n */, double *device_ms);
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------------- */
 adsb_status adsb_comm_unique_id(uint8_t id[128]);
 adsb_status adsb_comm_init(int nranks, int rank, const uint8_t id[128], int device, adsb_comm **out);

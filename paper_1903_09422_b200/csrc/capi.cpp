@@ -349,6 +349,17 @@ adsb_status adsb_sample_frames(const adsb_graph* g, int device, uint64_t seed, u
     });
 }
 
+adsb_status adsb_exact_bc(const adsb_graph* g, int device, double* bc, double* device_ms) {
+    return guard([&] {
+        need(g, "graph");
+        need(bc, "bc");
+        if (g->host.n == 0) invalid("graph is empty");
+        Locked L = locked_context(g, device);
+        const double ms = device_exact_bc(L.ctx, bc);
+        if (device_ms) *device_ms = ms;
+    });
+}
+
 adsb_status adsb_comm_unique_id(uint8_t id[128]) {
     return guard([&] {
         need(id, "id");

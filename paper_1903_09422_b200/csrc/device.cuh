@@ -128,6 +128,7 @@ struct SamplerArena {
     DevBuf<uint32_t> queue;            // slots * n
     DevBuf<uint2> qrange;              // slots * n (offset, degree)
     DevBuf<uint32_t> tlev;             // slots * level_cap
+    DevBuf<uint32_t> dagq;             // block teams: slots * n t-side DAG lists (push rebuild, low-degree graphs)
     DevBuf<uint32_t> slot_tag;         // slots: generation tag of each region
     DevBuf<uint32_t> slot_busy;        // block teams: bitmap of regions lent to blocks
 };
@@ -185,6 +186,9 @@ uint32_t device_components(DeviceContext& ctx);
 uint64_t device_eccentricity(DeviceContext& ctx, uint32_t source);
 // graph.hpp:202-214 diameter_upper_bound (requires device_components first)
 uint64_t device_diameter_bound(DeviceContext& ctx);
+
+// exact normalised BC (Brandes, f64; brandes.cu); returns the kernel time in ms
+double device_exact_bc(DeviceContext& ctx, double* host_bc);
 
 int num_sms(int device);
 

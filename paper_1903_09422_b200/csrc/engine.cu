@@ -201,7 +201,8 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     size_t free_b = 0, total_b = 0;
     ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     // per region: state (16 B/vertex), queue (4), warp teams also ranges (8)
-    const uint64_t per_vertex = kind == SamplerKind::kWarp ? 16 + 4 + 8 : 16 + 4;
+    // (block teams: + 4 for the t-side DAG lists of the low-degree push rebuild)
+    const uint64_t per_vertex = kind == SamplerKind::kWarp ? 16 + 4 + 8 : 16 + 4 + 4;
     const uint64_t per_slot = static_cast<uint64_t>(cap_n) * per_vertex + static_cast<uint64_t>(cap_levels) * 4;
     const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
     const uint64_t resident = static_cast<uint64_t>(sms) * per_sm;
@@ -224,6 +225,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->state.alloc(slots * cap_n * 2);
     a->queue.alloc(slots * cap_n);
     if (kind == SamplerKind::kWarp) a->qrange.alloc(slots * cap_n);
+    else a->dagq.alloc(slots * cap_n);
     a->tlev.alloc(slots * cap_levels);
     a->slot_tag.alloc(slots);
     a->slot_busy.alloc((slots + 31) / 32);
@@ -253,6 +255,7 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.queue = a.queue.ptr;
     p.qrange = a.qrange.ptr;
     p.tlev = a.tlev.ptr;
+    p.dagq = a.dagq.ptr;
     p.slot_tag = a.slot_tag.ptr;
     p.slot_busy = a.slot_busy.ptr;
     p.blocks = a.blocks;

@@ -69,6 +69,7 @@ struct SamplerParams {
     uint32_t* queue;            // slots * n
     uint2* qrange;              // slots * n
     uint32_t* tlev;             // slots * level_cap
+    uint32_t* dagq;             // block teams: slots * n t-side DAG lists (low-degree push rebuild)
     uint32_t* slot_tag;         // slots
     uint32_t* slot_busy;        // block teams: region bitmap (fallback samples borrow a region)
     uint32_t blocks;            // block teams: shared-memory kernel grid

@@ -36,6 +36,7 @@ struct Shared {
     uint32_t lvl_ins[3];              //   hash reservations (shared-memory store),
     uint32_t lvl_met[3];              //   whether the frontiers met (any thread sets it)
     uint32_t s_cnt, t_cnt;            // queue fill: s-side from 0 up, t-side from the top down
+    uint32_t dag_cnt;                 // push rebuild: fill of the t-side DAG list
     uint32_t overflow;
     uint32_t tlev_small[kSmemLevels]; // t-level boundaries (shared-memory store)
     unsigned long long wlo[kBT / 32]; // backtrack: per-warp 65-bit candidate sums
@@ -196,6 +197,10 @@ struct SmemStore {
         if (xh | carry) atomicAdd(w + 1, xh + carry);
     }
     __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], 0x40u); }
+    __device__ void prefetch(uint32_t) const {}
+    static constexpr bool kHasDagQueue = false;
+    uint32_t* dq = nullptr;
+    __device__ bool set_dag_first(uint32_t slot) { return !(atomicOr(&km[slot], 0x40u) & 0x40u); }
     __device__ unsigned long long sigma(uint32_t slot) const { return sig[slot]; }
     __device__ bool queue_ok(uint32_t s_cnt, uint32_t t_cnt) const { return s_cnt + t_cnt <= qcap; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
@@ -206,32 +211,82 @@ struct SmemStore {
     }
 };
 
-// Per-block dense global state (stamped with a per-block generation tag).
-// kU: adjacency loads kept in flight per thread by for_edges (the global-only
-// kernel trades registers for memory-level parallelism).
+// Per-team dense global state, 2 words per vertex: (present << 32 | meta),
+// sigma. ADSB_GSTORE_CLEAR (default): a region is all-zero between samples;
+// each sample zeroes exactly the words it claimed (the queue lists them) at
+// its end. A claim is then ONE compare-and-swap against 0 (no load first),
+// and sigma is zero before the claim, so an s-side level claims and
+// accumulates sigma in one pass (kSigmaPreZeroed). The older tagged layout
+// (tag << 32 | meta, never cleared; a claim is a load plus a CAS against
+// the stale word, sigma zeroed by the claimer and accumulated in a second
+// pass) is kept for A/B builds (-DADSB_GSTORE_CLEAR=0).
+// kU: adjacency loads kept in flight per thread by for_edges.
+#ifndef ADSB_LOWDEG_PREFETCH
+#define ADSB_LOWDEG_PREFETCH 1
+#endif
+#ifndef ADSB_LOWDEG_COUNT
+#define ADSB_LOWDEG_COUNT 1
+#endif
+#ifndef ADSB_GSTORE_CLEAR
+#define ADSB_GSTORE_CLEAR 1
+#endif
 template <uint32_t kU>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
-    unsigned long long* st;  // 2 words per vertex: (tag << 32 | meta), sigma
+    static constexpr bool kClear = ADSB_GSTORE_CLEAR != 0;
+    static constexpr unsigned long long kPresent = 1ull << 32;
+    unsigned long long* st;  // 2 words per vertex: (present|tag << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* tlev;
+    uint32_t* dq;      // t-side DAG lists, level by level (push rebuild)
     uint32_t tag;
     uint32_t qcap;
     uint32_t level_cap;
+    bool blind;        // cleared layout: claim with a CAS alone (low-degree graphs)
 
     __device__ void begin(uint32_t) {}
+    // Cleared layout: zero the state of every vertex this sample claimed
+    // (both queue ends, meeting-level claims included). The caller's next
+    // barrier orders these stores before the region's next claims.
     template <class CtxT>
-    __device__ void end(CtxT&, Shared&) {}
+    __device__ void end(CtxT& C, Shared& s) {
+        if constexpr (kClear) {
+            __syncthreads();
+            const uint32_t ns = s.s_cnt, nt = s.t_cnt;
+            for (uint32_t i = C.tid; i < ns + nt; i += kBT) {
+                const uint32_t v = __ldcg(qv + (i < ns ? i : tpos(i - ns)));
+                __stcg(reinterpret_cast<ulonglong2*>(st) + v, make_ulonglong2(0ull, 0ull));
+            }
+            __syncthreads();
+        }
+    }
     __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
         const unsigned long long x = __ldcg(st + 2ull * v);
-        if (static_cast<uint32_t>(x >> 32) != tag) return kNone;
+        if (kClear ? x == 0ull : static_cast<uint32_t>(x >> 32) != tag) return kNone;
         meta = static_cast<uint32_t>(x);
         return v;
     }
     template <bool kReserve = true>
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
+        if constexpr (kClear) {
+            // Hub-heavy graphs: look first, so the many edges into an already
+            // claimed hub are plain loads, not a queue of same-address atomics
+            // (measured: a blind CAS makes C5 38% slower). Low-degree graphs
+            // have no hubs: one CAS, no load.
+            if (!blind) {
+                const unsigned long long x = __ldcg(st + 2ull * v);
+                if (x != 0ull) {
+                    meta = static_cast<uint32_t>(x);
+                    return v;
+                }
+            }
+            const unsigned long long prev = atomicCAS(st + 2ull * v, 0ull, kPresent | new_meta);
+            inserted = prev == 0ull;
+            meta = inserted ? new_meta : static_cast<uint32_t>(prev);
+            return v;
+        }
         unsigned long long x = __ldcg(st + 2ull * v);
         if (static_cast<uint32_t>(x >> 32) != tag) {
             const unsigned long long want = (static_cast<unsigned long long>(tag) << 32) | new_meta;
@@ -246,11 +301,18 @@ struct GlobalStoreT {
         meta = static_cast<uint32_t>(x);
         return v;
     }
-    static constexpr bool kSigmaPreZeroed = false;  // stale sigma: zero on claim, accumulate after a barrier
+    static constexpr bool kSigmaPreZeroed = kClear;  // tagged: stale sigma, zero on claim, accumulate after a barrier
     static constexpr bool kSpeculativeClaims = true;  // no capacity limit: probe and claim in one pass
-    __device__ void zero_sigma(uint32_t slot) { st[2ull * slot + 1] = 0ull; }
+    __device__ void zero_sigma(uint32_t slot) {
+        if constexpr (!kClear) st[2ull * slot + 1] = 0ull;
+    }
     __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(st + 2ull * slot + 1, x); }
     __device__ void set_dag(uint32_t slot) { atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)); }
+    __device__ void prefetch(uint32_t v) const { asm volatile("prefetch.global.L2 [%0];" ::"l"(st + 2ull * v)); }
+    static constexpr bool kHasDagQueue = true;
+    __device__ bool set_dag_first(uint32_t slot) {
+        return !(atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)) & kMetaDag);
+    }
     __device__ unsigned long long sigma(uint32_t slot) const { return __ldcg(st + 2ull * slot + 1); }
     __device__ bool queue_ok(uint32_t, uint32_t) const { return true; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
@@ -303,6 +365,37 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         // frontier vertex walks its whole adjacency; no scan, no chunk
         // barriers, one barrier per level. Imbalance is bounded by the max degree.
         unsigned long long mine = 0;
+#if ADSB_LOWDEG_PREFETCH
+        // Software pipeline over this thread's frontier vertices: the next
+        // vertex id is loaded and its CSR offsets prefetched while this one is
+        // processed, and the state words of this vertex's neighbours are
+        // prefetched into L2 before the first claim or probe touches them.
+        uint32_t i = lo + C.tid;
+        uint32_t u_next = i < hi ? S.qv[t_list ? S.tpos(i) : i] : 0u;
+        for (; i < hi; i += kBT) {
+            const uint32_t u = u_next;
+            const bool more = i + kBT < hi;
+            if (more) u_next = S.qv[t_list ? S.tpos(i + kBT) : i + kBT];
+            ADSB_DCHECK(u < C.n);
+            const uint32_t o = C.off[u], e = C.off[u + 1];
+            uint32_t meta;
+            const uint32_t slot = S.find(u, meta);
+            const unsigned long long val = prep(slot, meta, e - o);
+            mine += e - o;
+            for (uint32_t j0 = o; j0 < e; j0 += 4) {
+                uint32_t vv[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.nbrs[j0 + k] : kNone;
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    if (vv[k] != kNone) S.prefetch(vv[k]);
+                if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    if (vv[k] != kNone) body(slot, val, vv[k]);
+            }
+        }
+#else
         for (uint32_t i = lo + C.tid; i < hi; i += kBT) {
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
@@ -321,6 +414,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                     if (vv[k] != kNone) body(slot, val, vv[k]);
             }
         }
+#endif
         const uint32_t wm = __reduce_add_sync(kFull, static_cast<uint32_t>(mine));
         if (C.lane == 0 && wm) atomicAdd(counter, static_cast<unsigned long long>(wm));
         __syncthreads();
@@ -499,7 +593,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     __syncthreads();
     uint32_t s_lo = 0, s_hi = 1, t_lo = 0, t_hi = 1, a = 0, b = 0;
     uint32_t used = sh.lvl_ins[2];  // reservations so far (s and t)
-    unsigned long long deg_s = C.off[s + 1] - C.off[s], deg_t = C.off[t + 1] - C.off[t];
+    // Side balancing needs only an estimate of each frontier's work (any
+    // choice gives the same distances, sigma and DAG). Low-degree graphs on a
+    // store without a capacity limit use the frontier size and skip the
+    // per-level degree pass (a dependent offset load plus a barrier per level).
+    const bool by_count = ADSB_LOWDEG_COUNT && C.low_degree && S.room_for(~0ull);
+    unsigned long long deg_s = by_count ? 1ull : C.off[s + 1] - C.off[s];
+    unsigned long long deg_t = by_count ? 1ull : C.off[t + 1] - C.off[t];
     for (;;) {
         if (a >= Store::kMaxDist || b >= Store::kMaxDist) return {a, b, 1};  // deeper than the store encodes
         const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
@@ -549,7 +649,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             a += 1;
             if (C.tid == 0) sh.s_cnt = s_hi;
             if (s_lo == s_hi) return {a, b, 2};
-            deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
+            deg_s = by_count ? s_hi - s_lo : level_degrees(C, S, s_lo, s_hi, false, cur);
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
@@ -587,7 +687,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             }
             if (b + 2 > S.level_cap) return {a, b, 1};
             if (t_lo == t_hi) return {a, b, 2};
-            deg_t = level_degrees(C, S, t_lo, t_hi, true, cur);
+            deg_t = by_count ? t_hi - t_lo : level_degrees(C, S, t_lo, t_hi, true, cur);
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
@@ -637,7 +737,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             used += sh.lvl_ins[cur];
             a += 1;
             if (s_lo == s_hi) return {a, b, 2};
-            deg_s = level_degrees(C, S, s_lo, s_hi, false, cur);
+            deg_s = by_count ? s_hi - s_lo : level_degrees(C, S, s_lo, s_hi, false, cur);
         } else {
             // ---- t-side level b: probe for the s-ball
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
@@ -678,7 +778,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (C.tid == 0 && b + 2 <= S.level_cap) S.tlev[b + 1] = t_hi;
             if (b + 2 > S.level_cap) return {a, b, 1};
             if (t_lo == t_hi) return {a, b, 2};
-            deg_t = level_degrees(C, S, t_lo, t_hi, true, cur);
+            deg_t = by_count ? t_hi - t_lo : level_degrees(C, S, t_lo, t_hi, true, cur);
         }
     }
 }
@@ -698,6 +798,60 @@ __device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
                       }
                   });
     }
+}
+
+// Push form for low-degree graphs on the global store: only the t-side DAG
+// is walked. The DAG vertices of T_b are listed first (one pass over T_b);
+// then each listed vertex x of T_k adds sigma(x) to its T_{k-1} neighbours
+// and lists the ones it flags first. A lattice's DAG is ~20% of its t-ball,
+// which the pull form reads whole. Same sums mod 2^64, same flags.
+#ifndef ADSB_PUSH_REBUILD
+#define ADSB_PUSH_REBUILD 1
+#endif
+template <class Store>
+__device__ void rebuild_push(Ctx& C, Store& S, uint32_t b) {
+    Shared& sh = *C.sh;
+    if (C.tid == 0) sh.dag_cnt = 0;
+    __syncthreads();
+    for (uint32_t j = S.tlev[b] + C.tid; j < S.tlev[b + 1]; j += kBT) {
+        const uint32_t v = __ldcg(S.qv + S.tpos(j));
+        uint32_t m;
+        const bool dag = S.find(v, m) != kNone && (m & kMetaDag);
+        if (dag) S.dq[aggregated_inc(&sh.dag_cnt)] = v;
+    }
+    __syncthreads();
+    uint32_t lo = 0, hi = sh.dag_cnt;
+    unsigned long long scanned = 0;
+    for (uint32_t k = b; k >= 1; --k) {
+        for (uint32_t i = lo + C.tid; i < hi; i += kBT) {
+            const uint32_t x = __ldcg(S.dq + i);
+            const unsigned long long sx = S.sigma(x);
+            const uint32_t o = C.off[x], e = C.off[x + 1];
+            scanned += e - o;
+            for (uint32_t j0 = o; j0 < e; j0 += 4) {
+                uint32_t ww[4];
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) ww[q] = j0 + q < e ? C.nbrs[j0 + q] : kNone;
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q)
+                    if (ww[q] != kNone) S.prefetch(ww[q]);
+#pragma unroll
+                for (uint32_t q = 0; q < 4; ++q) {
+                    if (ww[q] == kNone) continue;
+                    uint32_t m;
+                    if (S.find(ww[q], m) == kNone || !m_is_t(m) || m_dist(m) != k - 1) continue;
+                    S.add_sigma(ww[q], sx);
+                    if (!(m & kMetaDag) && S.set_dag_first(ww[q])) S.dq[aggregated_inc(&sh.dag_cnt)] = ww[q];
+                }
+            }
+        }
+        __syncthreads();
+        lo = hi;
+        hi = sh.dag_cnt;
+    }
+    const uint32_t wm = __reduce_add_sync(kFull, static_cast<uint32_t>(scanned));
+    if (C.lane == 0 && wm) atomicAdd(&sh.st_rebuild, static_cast<unsigned long long>(wm));
+    __syncthreads();
 }
 
 __device__ __forceinline__ void add65(unsigned long long& lo, uint32_t& hi, unsigned long long xlo, uint32_t xhi) {
@@ -959,7 +1113,12 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         S.end(C, *C.sh);
         return mt.status;
     }
-    rebuild(C, S, mt.b);
+    if constexpr (Store::kHasDagQueue && ADSB_PUSH_REBUILD) {
+        if (C.low_degree) rebuild_push(C, S, mt.b);
+        else rebuild(C, S, mt.b);
+    } else {
+        rebuild(C, S, mt.b);
+    }
     ADSB_PHASE_MARK(t2);
     const int rc = backtrack<kMode>(C, S, p, rng, t, mt, frame_local) ? 0 : 2;  // block-uniform
     ADSB_PHASE_MARK(t3);
@@ -999,6 +1158,8 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
+    gs.dq = p.dagq + static_cast<size_t>(p.slot_stride) * slot;
+    gs.blind = p.max_degree <= 32;
     gs.tag = tag;
     gs.qcap = p.n;
     gs.level_cap = p.level_cap;

@@ -142,5 +142,16 @@ def sample_frames(g: Graph, seed: int, samples_per_frame: int, first: int, count
     return [incs[int(offsets[i]):int(offsets[i + 1])].copy() for i in range(count)]
 
 
+def exact_bc(g: Graph, device: int = -1) -> tuple[np.ndarray, float]:
+    """Exact betweenness of every vertex on the device (Brandes, f64), normalised by
+    n(n-1) like BcResult::scores; the validation the reference runs with ApspOracle
+    (tests/test_util.hpp:164-206). Returns (scores, kernel milliseconds)."""
+    n = g.num_vertices()
+    out = np.zeros(n, dtype=np.float64)
+    ms = C.c_double(0.0)
+    check(lib().adsb_exact_bc(g.handle, device, out.ctypes.data_as(dblp), C.byref(ms)))
+    return out, ms.value
+
+
 __all__ = ["allocate_deltas", "compute_omega", "f_bound", "g_bound", "kadabra_check", "StopReason",
-           "to_string", "BcResult", "estimate_bc", "sample_frames", "Variant"]
+           "to_string", "BcResult", "estimate_bc", "exact_bc", "sample_frames", "Variant"]

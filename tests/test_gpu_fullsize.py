@@ -1,0 +1,137 @@
+"""GPU parity at BASELINE.json sizes and against exact betweenness.
+
+The oracle finishes only small cases in seconds, so the full-size configs are
+checked through size-independent properties:
+
+* exact BC on the device (Brandes, f64; kadabra.exact_bc) first agrees with the
+  oracle's Brandes (oracle.c or_brandes) to rounding on small graphs;
+* the (eps, delta) guarantee: every estimate within eps of exact BC on an
+  R-MAT graph of C2's shape (scale 16), deterministic and cumulative-epoch
+  modes (tolerance = eps, written in the test);
+* C2 at full size: the cumulative-epoch (non-det) estimate within eps of the
+  deterministic (indexed-frame) estimate, which is the reference's own output
+  (bit-exact against the oracle / compiled reference on every smaller graph);
+* C3 at full size: the deterministic result is the same with every sampler
+  store (shared-memory table, global state, 128-thread blocks), and its first
+  frames equal the oracle's;
+* a deep, low-degree lattice with holes (C4's shape, smaller): sampled paths
+  equal the oracle's on the global-state store with thread-per-vertex
+  expansion.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1903_09422_b200 import adsamp, datasets
+from paper_1903_09422_b200.adsamp import EngineConfig, Variant
+from paper_1903_09422_b200.kadabra import estimate_bc, exact_bc, sample_frames
+
+from conftest import SMALL_GRAPHS
+
+pytestmark = pytest.mark.gpu
+
+
+def both(pairs):
+    return adsamp.graph_from_pairs(pairs), oracle.from_pairs(pairs)
+
+
+RMAT = dict(a=0.57, b=0.19, c=0.19)
+
+
+@pytest.mark.parametrize("name", ["path3", "star4", "cycle4", "cube", "k23", "er100", "two_components", "c1", "rmat11"])
+def test_exact_bc_matches_oracle_brandes(name):
+    if name == "c1":
+        pairs = datasets.pairs("c1_er")
+    elif name == "rmat11":
+        pairs = datasets.gen_rmat(11, 16, RMAT["a"], RMAT["b"], RMAT["c"], 5)
+    else:
+        pairs = SMALL_GRAPHS[name]()
+    pg, og = both(pairs)
+    got, ms = exact_bc(pg.graph, device=0)
+    want = oracle.brandes(og)
+    assert ms >= 0.0
+    np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-15)
+
+
+@pytest.fixture(scope="module")
+def rmat16():
+    pairs = datasets.gen_rmat(16, 16, RMAT["a"], RMAT["b"], RMAT["c"], 16)
+    pg = adsamp.graph_from_pairs(pairs)
+    exact, _ = exact_bc(pg.graph, device=0)
+    return pg, exact
+
+
+@pytest.mark.parametrize("variant", [Variant.indexed, Variant.shared])
+def test_estimates_within_eps_of_exact_rmat16(rmat16, variant):
+    pg, exact = rmat16
+    eps = 0.005
+    cfg = EngineConfig(variant=variant, samples_per_frame=1, threads=8, base_seed=42, device=0)
+    r = estimate_bc(pg.graph, eps, 0.1, cfg)
+    assert r.reason.name == "eps_converged"
+    err = np.max(np.abs(r.scores - exact))
+    assert err <= eps, f"max |estimate - exact| = {err} > eps = {eps}"
+
+
+def test_c2_fullsize_nondet_within_eps_of_deterministic():
+    w = datasets.CONFIGS["c2_rmat18"]
+    g = datasets.graph("c2_rmat18").graph
+    det = estimate_bc(g, w.epsilon, w.delta,
+                      EngineConfig(variant=Variant.indexed, samples_per_frame=1, threads=8, base_seed=42, device=0))
+    nd = estimate_bc(g, w.epsilon, w.delta,
+                     EngineConfig(variant=Variant.shared, threads=8, base_seed=42, device=0))
+    nd2 = estimate_bc(g, w.epsilon, w.delta,
+                      EngineConfig(variant=Variant.shared, threads=8, base_seed=42, device=0))
+    # epochs are index ranges: the non-det mode is reproducible run to run
+    assert nd.tau == nd2.tau
+    np.testing.assert_array_equal(nd.run.data, nd2.run.data)
+    assert det.reason.name == nd.reason.name == "eps_converged"
+    assert np.max(np.abs(nd.scores - det.scores)) <= w.epsilon
+    # every sample credits d(s,t)-1 interior vertices: counts are bounded by tau each
+    assert int(nd.run.data.max()) <= nd.tau and int(det.run.data.max()) <= det.tau
+
+
+@pytest.mark.parametrize("mode", ["block-global", "block-128"])
+def test_c3_fullsize_deterministic_store_invariance(mode, monkeypatch):
+    w = datasets.CONFIGS["c3_ba"]
+    pairs = datasets.pairs("c3_ba")
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=1, threads=8, base_seed=w.seed, device=0)
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    monkeypatch.delenv("ADSB_BLOCK", raising=False)
+    ref = estimate_bc(adsamp.graph_from_pairs(pairs).graph, w.epsilon, w.delta, cfg)
+    if mode == "block-global":
+        monkeypatch.setenv("ADSB_NO_SMEM", "1")
+    else:
+        monkeypatch.setenv("ADSB_BLOCK", "128")
+    got = estimate_bc(adsamp.graph_from_pairs(pairs).graph, w.epsilon, w.delta, cfg)
+    assert (got.tau, got.run.check_cycles, got.reason.name) == (ref.tau, ref.run.check_cycles, ref.reason.name)
+    np.testing.assert_array_equal(got.run.data, ref.run.data)
+
+
+def test_c3_fullsize_first_frames_match_oracle():
+    pairs = datasets.pairs("c3_ba")
+    pg, og = both(pairs)
+    got = sample_frames(pg.graph, 42, 1, 0, 24, device=0)
+    want = oracle.sample_frames(og, 42, 1, 0, 24)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", ["global", "auto"])
+def test_holey_lattice_lowdegree_frames(mode, monkeypatch):
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    if mode == "global":
+        monkeypatch.setenv("ADSB_NO_SMEM", "1")
+    else:
+        monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    pairs = datasets.gen_grid(300, 300, 0.1, 5)
+    pg, og = both(pairs)
+    got = sample_frames(pg.graph, 11, 2, 3, 60, device=0)
+    want = oracle.sample_frames(og, 11, 2, 3, 60)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=1, threads=8, base_seed=11, max_cycles=500, device=0)
+    r = estimate_bc(pg.graph, 0.02, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.02, 0.1, spf=1, seed=11, nominal_threads=8, max_frames=500)
+    assert (r.tau, r.run.check_cycles) == (o.tau, o.check_cycles)
+    np.testing.assert_array_equal(r.run.data, o.counts)
