@@ -243,5 +243,13 @@ inline BcResult estimate_bc(const Graph& g, double epsilon, double delta, const 
     return r;
 }
 
+// Exact normalised BC on the device (Brandes, f64): the validation the
+// reference runs with ApspOracle (tests/test_util.hpp:164-206), at C2's size.
+inline std::vector<double> exact_bc(const Graph& g, int device = -1) {
+    std::vector<double> bc(g.num_vertices());
+    detail::check(adsb_exact_bc(g.handle(), device, bc.data(), nullptr));
+    return bc;
+}
+
 }  // namespace kadabra
 }  // namespace adsamp_b200

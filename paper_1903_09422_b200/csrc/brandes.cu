@@ -203,10 +203,13 @@ double device_exact_bc(DeviceContext& ctx, double* host_bc) {
     p.delta = delta.ptr;
     p.order = order.ptr;
     p.bc = bc.ptr;
-    ADSB_CUDA(cudaEventRecord(rt.ev_a, st));
+    cudaEvent_t ev0, ev1;
+    ADSB_CUDA(cudaEventCreate(&ev0));
+    ADSB_CUDA(cudaEventCreate(&ev1));
+    ADSB_CUDA(cudaEventRecord(ev0, st));
     brandes_kernel<<<static_cast<unsigned>(blocks), kBT, 0, st>>>(p);
     ADSB_CUDA(cudaGetLastError());
-    ADSB_CUDA(cudaEventRecord(rt.ev_b, st));
+    ADSB_CUDA(cudaEventRecord(ev1, st));
     const double pairs = static_cast<double>(n) * static_cast<double>(n - 1);
     reduce_bc<<<static_cast<unsigned>(num_sms(ctx.device) * 8), 256, 0, st>>>(bc.ptr, static_cast<uint32_t>(blocks), n,
                                                       n > 1 ? 1.0 / pairs : 0.0, out.ptr);
@@ -214,7 +217,9 @@ double device_exact_bc(DeviceContext& ctx, double* host_bc) {
     ADSB_CUDA(cudaMemcpyAsync(host_bc, out.ptr, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, st));
     ADSB_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
-    ADSB_CUDA(cudaEventElapsedTime(&ms, rt.ev_a, rt.ev_b));
+    ADSB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     return ms;
 }
 

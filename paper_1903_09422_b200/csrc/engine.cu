@@ -187,8 +187,18 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     DeviceRuntime& rt = *ctx.rt;
     rt.active = k;
     std::unique_ptr<SamplerArena>& slot = rt.arena[k];
+    // Global-state layout (sampler_cta_body.cuh GlobalStoreT): cleared words
+    // for low-degree graphs, generation tags otherwise. Regions hold the other
+    // layout's leftovers after a switch, so the state is zeroed then.
+    const int layout = k == 1 && ctx.graph.max_degree <= 32 && !std::getenv("ADSB_TAGGED") ? 1 : 0;
     if (slot && slot->n >= n && slot->level_cap >= level_cap && slot->hash_cap == hash_cap &&
         slot->block_threads == block_threads) {
+        if (slot->layout != layout) {
+            ADSB_CUDA(cudaMemsetAsync(slot->state.ptr, 0, slot->state.bytes(), rt.stream));
+            ADSB_CUDA(cudaMemsetAsync(slot->slot_tag.ptr, 0, slot->slot_tag.bytes(), rt.stream));
+            ADSB_CUDA(cudaStreamSynchronize(rt.stream));
+            slot->layout = layout;
+        }
         return;
     }
     const uint32_t cap_n = slot ? std::max(slot->n, n) : n;
@@ -215,6 +225,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->kind = k;
     a->hash_cap = hash_cap;
     a->block_threads = block_threads;
+    a->layout = layout;
     a->slots = static_cast<uint32_t>(slots);
     // Block teams launch every resident block for the shared-memory kernels
     // even when fewer global regions fit (huge graphs): a sample that
@@ -255,6 +266,14 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.queue = a.queue.ptr;
     p.qrange = a.qrange.ptr;
     p.tlev = a.tlev.ptr;
+    p.clear_layout = static_cast<uint32_t>(a.layout);
+    {
+        int l2 = 0;
+        ADSB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx.device));
+        const uint64_t csr = 4ull * (ctx.graph.n + 1) + 4ull * ctx.graph.nnz;
+        p.csr_hint = csr * 2 <= static_cast<uint64_t>(l2) ? 1.0f : 0.0f;
+        if (const char* e = std::getenv("ADSB_CSR_HINT")) p.csr_hint = std::strtof(e, nullptr);
+    }
     p.dagq = a.dagq.ptr;
     p.slot_tag = a.slot_tag.ptr;
     p.slot_busy = a.slot_busy.ptr;

@@ -179,7 +179,7 @@ struct SmemStore {
             h = h + 1 < cap ? h + 1 : 0u;
         }
     }
-    static constexpr bool kSigmaPreZeroed = true;  // claim and sigma accumulation share one pass
+    __device__ static constexpr bool pre_zeroed() { return true; }  // claim and sigma accumulation share one pass
     static constexpr bool kSpeculativeClaims = false;  // meeting-level claims would overflow the table
     __device__ void zero_sigma(uint32_t) {}
     // 64-bit shared-memory atomics are CAS loops on sm_100; sigma (mod 2^64)
@@ -198,6 +198,11 @@ struct SmemStore {
     }
     __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], 0x40u); }
     __device__ void prefetch(uint32_t) const {}
+    __device__ unsigned long long claim_issue(uint32_t, uint32_t) { return ~0ull; }
+    template <bool kReserve = true>
+    __device__ uint32_t claim_tok(uint32_t v, uint32_t new_meta, unsigned long long, bool& inserted, uint32_t& meta) {
+        return claim<kReserve>(v, new_meta, inserted, meta);
+    }
     static constexpr bool kHasDagQueue = false;
     uint32_t* dq = nullptr;
     __device__ bool set_dag_first(uint32_t slot) { return !(atomicOr(&km[slot], 0x40u) & 0x40u); }
@@ -211,15 +216,21 @@ struct SmemStore {
     }
 };
 
-// Per-team dense global state, 2 words per vertex: (present << 32 | meta),
-// sigma. ADSB_GSTORE_CLEAR (default): a region is all-zero between samples;
-// each sample zeroes exactly the words it claimed (the queue lists them) at
-// its end. A claim is then ONE compare-and-swap against 0 (no load first),
-// and sigma is zero before the claim, so an s-side level claims and
-// accumulates sigma in one pass (kSigmaPreZeroed). The older tagged layout
-// (tag << 32 | meta, never cleared; a claim is a load plus a CAS against
-// the stale word, sigma zeroed by the claimer and accumulated in a second
-// pass) is kept for A/B builds (-DADSB_GSTORE_CLEAR=0).
+// Per-team dense global state, 2 words per vertex, in one of two layouts
+// chosen per graph (SamplerParams::clear_layout; the engine zeroes the arena
+// when a graph switches it):
+//  * tagged (hub-heavy graphs): word 0 = tag << 32 | meta with a per-sample
+//    generation tag, never cleared. A claim loads the word and CASes it
+//    against the stale value, so the many edges into an already-claimed hub
+//    are plain loads. The claimer zeroes sigma; an s-side level accumulates
+//    sigma in a second pass (skipped on the meeting level, the biggest one).
+//  * cleared (low-degree graphs, e.g. lattices): word 0 = present << 32 |
+//    meta, and a region is all-zero between samples: each sample zeroes the
+//    words it claimed (both queue ends) at its end. A claim is ONE CAS
+//    against 0 with no load first, and sigma is already zero, so an s-side
+//    level claims and accumulates in one pass. Measured on C4: -22% with the
+//    push rebuild; on C3/C5 the blind CAS and one-pass sums cost 15-35%
+//    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
 #ifndef ADSB_LOWDEG_PREFETCH
 #define ADSB_LOWDEG_PREFETCH 1
@@ -227,23 +238,19 @@ struct SmemStore {
 #ifndef ADSB_LOWDEG_COUNT
 #define ADSB_LOWDEG_COUNT 1
 #endif
-#ifndef ADSB_GSTORE_CLEAR
-#define ADSB_GSTORE_CLEAR 1
-#endif
 template <uint32_t kU>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
-    static constexpr bool kClear = ADSB_GSTORE_CLEAR != 0;
     static constexpr unsigned long long kPresent = 1ull << 32;
-    unsigned long long* st;  // 2 words per vertex: (present|tag << 32 | meta), sigma
+    unsigned long long* st;  // 2 words per vertex: (tag or present << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* tlev;
     uint32_t* dq;      // t-side DAG lists, level by level (push rebuild)
     uint32_t tag;
     uint32_t qcap;
     uint32_t level_cap;
-    bool blind;        // cleared layout: claim with a CAS alone (low-degree graphs)
+    bool clear;        // cleared layout (see above)
 
     __device__ void begin(uint32_t) {}
     // Cleared layout: zero the state of every vertex this sample claimed
@@ -251,7 +258,7 @@ struct GlobalStoreT {
     // barrier orders these stores before the region's next claims.
     template <class CtxT>
     __device__ void end(CtxT& C, Shared& s) {
-        if constexpr (kClear) {
+        if (clear) {
             __syncthreads();
             const uint32_t ns = s.s_cnt, nt = s.t_cnt;
             for (uint32_t i = C.tid; i < ns + nt; i += kBT) {
@@ -263,25 +270,14 @@ struct GlobalStoreT {
     }
     __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
         const unsigned long long x = __ldcg(st + 2ull * v);
-        if (kClear ? x == 0ull : static_cast<uint32_t>(x >> 32) != tag) return kNone;
+        if (clear ? x == 0ull : static_cast<uint32_t>(x >> 32) != tag) return kNone;
         meta = static_cast<uint32_t>(x);
         return v;
     }
     template <bool kReserve = true>
     __device__ uint32_t claim(uint32_t v, uint32_t new_meta, bool& inserted, uint32_t& meta) {
         inserted = false;
-        if constexpr (kClear) {
-            // Hub-heavy graphs: look first, so the many edges into an already
-            // claimed hub are plain loads, not a queue of same-address atomics
-            // (measured: a blind CAS makes C5 38% slower). Low-degree graphs
-            // have no hubs: one CAS, no load.
-            if (!blind) {
-                const unsigned long long x = __ldcg(st + 2ull * v);
-                if (x != 0ull) {
-                    meta = static_cast<uint32_t>(x);
-                    return v;
-                }
-            }
+        if (clear) {
             const unsigned long long prev = atomicCAS(st + 2ull * v, 0ull, kPresent | new_meta);
             inserted = prev == 0ull;
             meta = inserted ? new_meta : static_cast<uint32_t>(prev);
@@ -301,10 +297,25 @@ struct GlobalStoreT {
         meta = static_cast<uint32_t>(x);
         return v;
     }
-    static constexpr bool kSigmaPreZeroed = kClear;  // tagged: stale sigma, zero on claim, accumulate after a barrier
+    // Batched low-degree claims: the CAS is issued early (claim_issue) and
+    // its old word decoded later (claim_tok); otherwise claim_tok claims.
+    __device__ unsigned long long claim_issue(uint32_t v, uint32_t new_meta) {
+        if (clear) return atomicCAS(st + 2ull * v, 0ull, kPresent | new_meta);
+        return ~0ull;
+    }
+    template <bool kReserve = true>
+    __device__ uint32_t claim_tok(uint32_t v, uint32_t new_meta, unsigned long long tok, bool& inserted,
+                                  uint32_t& meta) {
+        if (tok == ~0ull) return claim<kReserve>(v, new_meta, inserted, meta);
+        inserted = tok == 0ull;
+        meta = inserted ? new_meta : static_cast<uint32_t>(tok);
+        return v;
+    }
+    // sigma is zero before the claim, so claims and sums share one pass
+    __device__ bool pre_zeroed() const { return clear; }
     static constexpr bool kSpeculativeClaims = true;  // no capacity limit: probe and claim in one pass
     __device__ void zero_sigma(uint32_t slot) {
-        if constexpr (!kClear) st[2ull * slot + 1] = 0ull;
+        if (!clear) st[2ull * slot + 1] = 0ull;
     }
     __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(st + 2ull * slot + 1, x); }
     __device__ void set_dag(uint32_t slot) { atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)); }
@@ -320,9 +331,22 @@ struct GlobalStoreT {
     __device__ void set_level(uint32_t*, uint32_t) {}
 };
 
+// CSR reads carry an L2 eviction-priority hint: evict_last when the CSR fits
+// in a fraction of L2 (SamplerParams::csr_hint = 1), so the per-sample state
+// streaming through L2 (C4: ~10 GB per 1k samples) does not evict it.
+__device__ __forceinline__ uint32_t ld_csr(const uint32_t* p, float frac) {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
 struct Ctx {
     const uint32_t* __restrict__ off;
     const uint32_t* __restrict__ nbrs;
+    float csr_hint;
+    __device__ __forceinline__ uint32_t O(size_t i) const { return ld_csr(off + i, csr_hint); }
+    __device__ __forceinline__ uint32_t N(size_t i) const { return ld_csr(nbrs + i, csr_hint); }
     uint32_t tid;
     uint32_t lane;
     uint32_t warp;
@@ -355,9 +379,17 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 // Visit the flattened adjacency of queue entries [lo, hi) (t-side entries when
 // t_list). prep(slot) gives the per-vertex payload; body(slot_u, payload, v)
 // runs once per adjacency entry. Ends with a block barrier.
-template <class Store, class Prep, class Body>
-__device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long* counter,
-                          Prep prep, Body body) {
+// for_edges_tok: issue(v) runs for a low-degree vertex's (up to 4)
+// neighbours before any body, and its token is passed to body(.., v, tok):
+// claims issue their compare-and-swaps together (ADSB_LOWDEG_BATCH) instead
+// of one dependent round trip per neighbour.
+#ifndef ADSB_LOWDEG_BATCH
+#define ADSB_LOWDEG_BATCH 0
+#endif
+constexpr unsigned long long kNoTok = ~0ull;
+template <class Store, class Prep, class Issue, class Body>
+__device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long* counter,
+                              Prep prep, Issue issue, Body body) {
     Shared& sh = *C.sh;
     ADSB_PHASE_ADD(6, 1);
     if (C.low_degree) {
@@ -377,7 +409,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             const bool more = i + kBT < hi;
             if (more) u_next = S.qv[t_list ? S.tpos(i + kBT) : i + kBT];
             ADSB_DCHECK(u < C.n);
-            const uint32_t o = C.off[u], e = C.off[u + 1];
+            const uint32_t o = C.O(u), e = C.O(u + 1);
             uint32_t meta;
             const uint32_t slot = S.find(u, meta);
             const unsigned long long val = prep(slot, meta, e - o);
@@ -385,14 +417,24 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             for (uint32_t j0 = o; j0 < e; j0 += 4) {
                 uint32_t vv[4];
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.nbrs[j0 + k] : kNone;
+                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.N(j0 + k) : kNone;
+#if ADSB_LOWDEG_BATCH
+                unsigned long long tok[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) tok[k] = vv[k] != kNone ? issue(vv[k]) : kNoTok;
+                if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    if (vv[k] != kNone) body(slot, val, vv[k], tok[k]);
+#else
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
                     if (vv[k] != kNone) S.prefetch(vv[k]);
                 if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
-                    if (vv[k] != kNone) body(slot, val, vv[k]);
+                    if (vv[k] != kNone) body(slot, val, vv[k], kNoTok);
+#endif
             }
         }
 #else
@@ -400,7 +442,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
             ADSB_DCHECK(u < C.n);
-            const uint32_t o = C.off[u], e = C.off[u + 1];
+            const uint32_t o = C.O(u), e = C.O(u + 1);
             uint32_t meta;
             const uint32_t slot = S.find(u, meta);
             const unsigned long long val = prep(slot, meta, e - o);
@@ -408,10 +450,10 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             for (uint32_t j0 = o; j0 < e; j0 += 4) {
                 uint32_t vv[4];
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.nbrs[j0 + k] : kNone;
+                for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.N(j0 + k) : kNone;
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k)
-                    if (vv[k] != kNone) body(slot, val, vv[k]);
+                    if (vv[k] != kNone) body(slot, val, vv[k], kNoTok);
             }
         }
 #endif
@@ -429,8 +471,8 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
             ADSB_DCHECK(u < C.n);
-            o = C.off[u];
-            deg = C.off[u + 1] - o;
+            o = C.O(u);
+            deg = C.O(u + 1) - o;
             uint32_t meta;
             slot = S.find(u, meta);
             val = prep(slot, meta, deg);
@@ -482,7 +524,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                         o_base = sh.cbase[ow];
                         have = true;
                     }
-                    vv[k] = C.nbrs[o_base + e];
+                    vv[k] = C.N(o_base + e);
                     // pull this thread's next adjacency id into L1 while the
                     // body runs (same row: the common case inside hub lists)
                     if (k + 1 == kBatch && e + kBT < o_end)
@@ -497,7 +539,7 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
                 ADSB_DCHECK(v < C.n);
                 const uint32_t w = owners & 0xFFu;
                 owners >>= 8;
-                body(sh.cslot[w], sh.cval[w], v);
+                body(sh.cslot[w], sh.cval[w], v, kNoTok);
 #pragma unroll
                 for (uint32_t j = 0; j + 1 < kBatch; ++j) vv[j] = vv[j + 1];
             }
@@ -508,6 +550,13 @@ __device__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_lis
         ADSB_PHASE_ADD(9, f2 - f1);
         ADSB_PHASE_ADD(11, f3 - f2);
     }
+}
+
+template <class Store, class Prep, class Body>
+__device__ __forceinline__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list,
+                                          unsigned long long* counter, Prep prep, Body body) {
+    for_edges_tok(C, S, lo, hi, t_list, counter, prep, [](uint32_t) { return kNoTok; },
+                  [&](uint32_t su, unsigned long long val, uint32_t v, unsigned long long) { body(su, val, v); });
 }
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int src) {
@@ -548,8 +597,8 @@ __device__ uint32_t level_degrees(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bo
         uint32_t lo_off[4], hi_off[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            lo_off[k] = v[k] != kNone ? C.off[v[k]] : 0u;
-            hi_off[k] = v[k] != kNone ? C.off[v[k] + 1] : 0u;
+            lo_off[k] = v[k] != kNone ? C.O(v[k]) : 0u;
+            hi_off[k] = v[k] != kNone ? C.O(v[k] + 1) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) my += hi_off[k] - lo_off[k];
@@ -598,8 +647,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     // store without a capacity limit use the frontier size and skip the
     // per-level degree pass (a dependent offset load plus a barrier per level).
     const bool by_count = ADSB_LOWDEG_COUNT && C.low_degree && S.room_for(~0ull);
-    unsigned long long deg_s = by_count ? 1ull : C.off[s + 1] - C.off[s];
-    unsigned long long deg_t = by_count ? 1ull : C.off[t + 1] - C.off[t];
+    unsigned long long deg_s = by_count ? 1ull : C.O(s + 1) - C.O(s);
+    unsigned long long deg_t = by_count ? 1ull : C.O(t + 1) - C.O(t);
     for (;;) {
         if (a >= Store::kMaxDist || b >= Store::kMaxDist) return {a, b, 1};  // deeper than the store encodes
         const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
@@ -609,15 +658,16 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
-            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges_tok(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
-                      [&](uint32_t, unsigned long long su, uint32_t v) {
+                      [&](uint32_t v) { return S.claim_issue(v, a + 1); },
+                      [&](uint32_t, unsigned long long su, uint32_t v, unsigned long long tok) {
                           bool ins;
                           uint32_t m;
-                          const uint32_t sl = S.template claim<false>(v, a + 1, ins, m);
+                          const uint32_t sl = S.template claim_tok<false>(v, a + 1, tok, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
-                              if (Store::kSigmaPreZeroed) S.add_sigma(sl, su);
+                              if (S.pre_zeroed()) S.add_sigma(sl, su);
                               const uint32_t pos = s_hi + aggregated_inc(&sh.lvl_cnt[cur]);
                               ADSB_DCHECK(pos + t_hi < S.qcap);
                               S.qv[pos] = v;
@@ -625,7 +675,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.add_sigma(sl, su);
                               if (!(m & kMetaDag)) S.set_dag(sl);
                               sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
-                          } else if (Store::kSigmaPreZeroed && !m_is_t(m) && m_dist(m) == a + 1) {
+                          } else if (S.pre_zeroed() && !m_is_t(m) && m_dist(m) == a + 1) {
                               S.add_sigma(sl, su);
                           }
                       });
@@ -635,7 +685,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                 if (C.tid == 0) sh.s_cnt = s_hi + added;  // the table clear walks the queue
                 return {a, b, 0};
             }
-            if (!Store::kSigmaPreZeroed)
+            if (!S.pre_zeroed())
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -654,12 +704,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
             const uint32_t meta_new = kMetaT | (b + 1);
-            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
+            for_edges_tok(C, S, t_lo, t_hi, true, &sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
-                      [&](uint32_t su_slot, unsigned long long, uint32_t v) {
+                      [&](uint32_t v) { return S.claim_issue(v, meta_new); },
+                      [&](uint32_t su_slot, unsigned long long, uint32_t v, unsigned long long tok) {
                           bool ins;
                           uint32_t m;
-                          const uint32_t sl = S.template claim<false>(v, meta_new, ins, m);
+                          const uint32_t sl = S.template claim_tok<false>(v, meta_new, tok, ins, m);
                           if (ins) {
                               S.zero_sigma(sl);
                               const uint32_t j = t_hi + aggregated_inc(&sh.lvl_cnt[cur]);
@@ -706,12 +757,12 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
-                      [&](uint32_t slot, uint32_t, uint32_t) { return Store::kSigmaPreZeroed ? S.sigma(slot) : 0ull; },
+                      [&](uint32_t slot, uint32_t, uint32_t) { return S.pre_zeroed() ? S.sigma(slot) : 0ull; },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           bool ins;
                           uint32_t m;
                           const uint32_t sl = S.claim(v, meta_new, ins, m);
-                          if (Store::kSigmaPreZeroed && sl != kNone && (ins || (!m_is_t(m) && m_dist(m) == a + 1)))
+                          if (S.pre_zeroed() && sl != kNone && (ins || (!m_is_t(m) && m_dist(m) == a + 1)))
                               S.add_sigma(sl, su);
                           if (ins) {
                               S.zero_sigma(sl);
@@ -724,7 +775,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
-            if (!Store::kSigmaPreZeroed)
+            if (!S.pre_zeroed())
             for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -826,12 +877,12 @@ __device__ void rebuild_push(Ctx& C, Store& S, uint32_t b) {
         for (uint32_t i = lo + C.tid; i < hi; i += kBT) {
             const uint32_t x = __ldcg(S.dq + i);
             const unsigned long long sx = S.sigma(x);
-            const uint32_t o = C.off[x], e = C.off[x + 1];
+            const uint32_t o = C.O(x), e = C.O(x + 1);
             scanned += e - o;
             for (uint32_t j0 = o; j0 < e; j0 += 4) {
                 uint32_t ww[4];
 #pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) ww[q] = j0 + q < e ? C.nbrs[j0 + q] : kNone;
+                for (uint32_t q = 0; q < 4; ++q) ww[q] = j0 + q < e ? C.N(j0 + q) : kNone;
 #pragma unroll
                 for (uint32_t q = 0; q < 4; ++q)
                     if (ww[q] != kNone) S.prefetch(ww[q]);
@@ -909,7 +960,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             want_t = false;
             want_dist = m_dist(cmeta) - 1;
         }
-        const uint32_t beg = C.off[cur], end = C.off[cur + 1];
+        const uint32_t beg = C.O(cur), end = C.O(cur + 1);
         bool found = false;
         if (end - beg <= kSmallStep) {
             // Low-degree step: warp 0 scans alone (warp-level 65-bit prefix),
@@ -923,7 +974,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                     unsigned long long val = 0;
                     bool cand = false;
                     if (i < end) {
-                        q = C.nbrs[i];
+                        q = C.N(i);
                         const uint32_t sl = S.find(q, m);
                         cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist &&
                                (!want_t || (m & kMetaDag));
@@ -968,12 +1019,12 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
         }
         // the next round's neighbour id is loaded one round ahead, so its
         // latency overlaps this round's barriers (hub steps take many rounds)
-        uint32_t q_next = !found && beg + C.tid < end ? C.nbrs[beg + C.tid] : 0u;
+        uint32_t q_next = !found && beg + C.tid < end ? C.N(beg + C.tid) : 0u;
         for (uint32_t base = beg; !found && base < end; base += kBT) {
             const uint32_t i = base + C.tid;
             uint32_t q = q_next, m = 0;
             unsigned long long val = 0;
-            if (i + kBT < end) q_next = C.nbrs[i + kBT];
+            if (i + kBT < end) q_next = C.N(i + kBT);
             if (i < end) {
                 const uint32_t sl = S.find(q, m);
                 if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag)))
@@ -1041,7 +1092,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                 uint32_t q = 0, m = 0;
                 bool cand = false;
                 if (i < end) {
-                    q = C.nbrs[i];
+                    q = C.N(i);
                     const uint32_t sl = S.find(q, m);
                     cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag));
                 }
@@ -1105,7 +1156,7 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 #ifdef ADSB_DEBUG_CHECKS
     if (mt.status == 0 && mt.a + mt.b == 0 && C.tid == 0) {
         bool adj = false;
-        for (uint32_t j = C.off[s]; j < C.off[s + 1]; ++j) adj |= C.nbrs[j] == t;
+        for (uint32_t j = C.O(s); j < C.O(s + 1); ++j) adj |= C.N(j) == t;
         ADSB_DCHECK(adj, "met at distance 1 but t is not a neighbour of s");
     }
 #endif
@@ -1159,7 +1210,7 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
     gs.dq = p.dagq + static_cast<size_t>(p.slot_stride) * slot;
-    gs.blind = p.max_degree <= 32;
+    gs.clear = p.clear_layout != 0;
     gs.tag = tag;
     gs.qcap = p.n;
     gs.level_cap = p.level_cap;
@@ -1341,6 +1392,7 @@ __global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
     Ctx C;
     C.off = p.off;
     C.nbrs = p.nbrs;
+    C.csr_hint = p.csr_hint;
     C.tid = threadIdx.x;
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
