@@ -281,6 +281,7 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.hash_cap = a.hash_cap;
     p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
     p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
+    if (const char* e = std::getenv("ADSB_GLOBAL_GRID")) p.global_grid = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     p.block_threads = a.block_threads;
     return p;
 }
