@@ -284,7 +284,13 @@ def main() -> None:
     prof = ROOT / "profiles" / "ncu_sampler_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(w.name, {}).get("dram_bytes_per_launch")
+            entry = json.loads(prof.read_text()).get(w.name, {})
+            traffic = entry.get("dram_bytes_per_launch")
+            if traffic is None and entry.get("dram_bytes_per_sample"):
+                # configs whose step launches several sampler batches: ncu bytes
+                # per sample (capped capture) x the samples of this step
+                traffic = entry["dram_bytes_per_sample"] * (
+                    sum(r.run.total_samples for r in results) / max(1, len(results)))
         except Exception:
             traffic = None
     launches = sum(r.kernel_launches for r in results)

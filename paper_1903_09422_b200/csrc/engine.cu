@@ -216,7 +216,12 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     const uint64_t per_slot = static_cast<uint64_t>(cap_n) * per_vertex + static_cast<uint64_t>(cap_levels) * 4;
     const uint64_t budget = static_cast<uint64_t>(static_cast<double>(free_b) * 0.55);
     const uint64_t resident = static_cast<uint64_t>(sms) * per_sm;
-    uint64_t slots = std::min<uint64_t>(resident, budget / std::max<uint64_t>(per_slot, 1));
+    // regions: enough for every resident block of the global-store-only kernel too
+    const uint64_t resident_regions =
+        kind == SamplerKind::kWarp ? resident
+                                   : std::max<uint64_t>(resident, static_cast<uint64_t>(sms) *
+                                                                      std::max(sampler_global_blocks_per_sm(), 1));
+    uint64_t slots = std::min<uint64_t>(resident_regions, budget / std::max<uint64_t>(per_slot, 1));
     if (kind == SamplerKind::kWarp) slots = slots / 8 * 8;
     if (slots < (kind == SamplerKind::kWarp ? 8u : 1u))
         fail(ADSB_ERR_CUDA, "not enough device memory for the sampler scratch (" +
@@ -281,6 +286,9 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.hash_cap = a.hash_cap;
     p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
     p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
+    // Low-degree graphs (cleared layout): 3 blocks per SM beat 4 (C4 -4%:
+    // fewer concurrent samples keep more of their frontier state in L2).
+    if (a.layout == 1) p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * 3);
     if (const char* e = std::getenv("ADSB_GLOBAL_GRID")) p.global_grid = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     p.block_threads = a.block_threads;
     return p;
@@ -706,7 +714,13 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         uint64_t max_epochs = (out.omega + B - 1) / B;
         if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
         max_epochs = std::max<uint64_t>(max_epochs, 1);
-        const uint32_t K = 8;
+        // Ring of K epoch slots: a block may start epoch e only after e - K was
+        // folded, and one slow sample holds its epoch's fold. K = 32 keeps
+        // the blocks busy through C5's long-tailed samples (K = 8: 23% of
+        // warp stall samples waited for a slot; C5 1.30 s -> 0.92 s to stop;
+        // profiles/r01_ab_round3.txt). Memory 8 B x K x n.
+        uint32_t K = 32;
+        if (const char* e = std::getenv("ADSB_RING_K")) K = std::min<uint32_t>(std::max<uint32_t>(std::strtoul(e, nullptr, 10), 2), 64);
         unsigned long long* ctl = ctx.rt->pool.get<unsigned long long>(Scratch::kCtl, kCtlWords);
         uint32_t* ring_cnt = ctx.rt->pool.get<uint32_t>(Scratch::kRingCnt, static_cast<size_t>(K) * n);
         uint32_t* ring_list = ctx.rt->pool.get<uint32_t>(Scratch::kRingList, static_cast<size_t>(K) * n);

@@ -38,6 +38,9 @@
 #ifndef ADSB_LOAD_BATCH
 #define ADSB_LOAD_BATCH 1  // adjacency loads in flight per thread in for_edges (A/B: 1 beats 2 and 4)
 #endif
+#ifndef ADSB_GLOBAL_MINB
+#define ADSB_GLOBAL_MINB 4  // min blocks/SM of the global-store-only kernel (256 threads; register budget)
+#endif
 #ifndef ADSB_MINB_PER_256
 #define ADSB_MINB_PER_256 4  // __launch_bounds__ min blocks for 256-thread blocks (register budget)
 #endif

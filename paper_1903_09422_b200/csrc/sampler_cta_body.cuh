@@ -1386,7 +1386,7 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
 }
 
 template <int kMode, bool kGlobalOnly>
-__global__ void __launch_bounds__(kBT, ADSB_MINB_PER_256 * 256 / kBT)
+__global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB : ADSB_MINB_PER_256 * 256 / kBT)
     sampler_cta_kernel(SamplerParams p) {
     __shared__ Shared sh;
     Ctx C;
