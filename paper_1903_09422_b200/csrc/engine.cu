@@ -242,7 +242,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->queue.alloc(slots * cap_n);
     if (kind == SamplerKind::kWarp) a->qrange.alloc(slots * cap_n);
     else a->dagq.alloc(slots * cap_n);
-    a->tlev.alloc(slots * cap_levels);
+    a->tlev.alloc(2 * slots * cap_levels);  // t-level then s-level boundaries per region
     a->slot_tag.alloc(slots);
     a->slot_busy.alloc((slots + 31) / 32);
     ADSB_CUDA(cudaMemsetAsync(a->slot_busy.ptr, 0, a->slot_busy.bytes(), rt.stream));

@@ -39,6 +39,7 @@ struct Shared {
     uint32_t dag_cnt;                 // push rebuild: fill of the t-side DAG list
     uint32_t overflow;
     uint32_t tlev_small[kSmemLevels]; // t-level boundaries (shared-memory store)
+    uint32_t slev_small[kSmemLevels]; // s-level boundaries (shared-memory store)
     unsigned long long wlo[kBT / 32]; // backtrack: per-warp 65-bit candidate sums
     uint32_t whi[kBT / 32];
     uint32_t first;                   // backtrack: first thread whose prefix exceeds r
@@ -69,6 +70,7 @@ struct SmemStore {
     uint32_t* km;
     uint32_t* qv;      // queue: vertex ids
     uint32_t* tlev;
+    uint32_t* slev;
     uint32_t cap;      // table entries (any size: slots come from a multiply-high)
     uint32_t qcap;
     uint32_t limit;    // max insertions (<= capacity/2 keeps probing short and finite)
@@ -232,6 +234,9 @@ struct SmemStore {
 //    push rebuild; on C3/C5 the blind CAS and one-pass sums cost 15-35%
 //    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
+#ifndef ADSB_LEVEL_PICK
+#define ADSB_LEVEL_PICK 1
+#endif
 #ifndef ADSB_LOWDEG_PREFETCH
 #define ADSB_LOWDEG_PREFETCH 1
 #endif
@@ -246,6 +251,7 @@ struct GlobalStoreT {
     unsigned long long* st;  // 2 words per vertex: (tag or present << 32 | meta), sigma
     uint32_t* qv;
     uint32_t* tlev;
+    uint32_t* slev;    // s-level boundaries (backtrack by level list)
     uint32_t* dq;      // t-side DAG lists, level by level (push rebuild)
     uint32_t tag;
     uint32_t qcap;
@@ -636,6 +642,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         S.qv[S.tpos(0)] = t;
         S.tlev[0] = 0;
         S.tlev[1] = 1;
+        S.slev[0] = 0;
+        S.slev[1] = 1;
         sh.s_cnt = 1;
         sh.t_cnt = 1;
     }
@@ -697,7 +705,10 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             s_hi += added;
             used += added;  // one-pass claims reserve nothing: occupancy grew by the inserts
             a += 1;
-            if (C.tid == 0) sh.s_cnt = s_hi;
+            if (C.tid == 0) {
+                sh.s_cnt = s_hi;
+                if (a + 2 <= S.level_cap) S.slev[a + 1] = s_hi;  // read only after later barriers
+            }
             if (s_lo == s_hi) return {a, b, 2};
             deg_s = by_count ? s_hi - s_lo : level_degrees(C, S, s_lo, s_hi, false, cur);
         } else if (deg_s > deg_t && S.room_for(deg_t)) {
@@ -787,6 +798,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             s_hi += added;
             used += sh.lvl_ins[cur];
             a += 1;
+            if (C.tid == 0 && a + 2 <= S.level_cap) S.slev[a + 1] = s_hi;
             if (s_lo == s_hi) return {a, b, 2};
             deg_s = by_count ? s_hi - s_lo : level_degrees(C, S, s_lo, s_hi, false, cur);
         } else {
@@ -932,6 +944,82 @@ __device__ __forceinline__ int pick_candidate(uint32_t cb, unsigned long long va
 // `r -= sigma[p]` scan. All threads draw the same r from their copy of the
 // stream. Returns false on an inconsistent state (every predecessor sigma
 // wrapped to 0), which the reference leaves undefined.
+// Hub steps: the predecessors of cur are exactly the vertices of one BFS
+// level list (s-level want_dist, or t-level want_dist with the DAG flag)
+// that are adjacent to cur. When that list is much shorter than N(cur), each
+// thread takes list entries and binary-searches them in cur's ascending
+// adjacency; the position found is the reference's scan order
+// (kadabra.hpp:231-241), so the candidates ranked by position with 65-bit
+// prefix sums pick the same predecessor as scanning N(cur). Returns false
+// (the caller scans) when more than kBT candidates turn up or no interval
+// holds r (every candidate sigma wrapped to 0).
+template <class Store>
+__device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_t lo, uint32_t hi, bool want_t,
+                           uint32_t want_dist, unsigned long long r, uint32_t& cur, uint32_t& cmeta,
+                           unsigned long long& csig) {
+    Shared& sh = *C.sh;
+    if (C.tid == 0) sh.dag_cnt = 0;
+    __syncthreads();
+    uint32_t probes = 0;
+    for (uint32_t j = lo + C.tid; j < hi; j += kBT) {
+        const uint32_t q = S.qv[want_t ? S.tpos(j) : j];
+        uint32_t m;
+        const uint32_t sl = S.find(q, m);
+        if (sl == kNone || m_is_t(m) != want_t || m_dist(m) != want_dist || (want_t && !(m & kMetaDag))) continue;
+        uint32_t l = beg, h = end;
+        while (l < h) {
+            const uint32_t mid = (l + h) >> 1;
+            ++probes;
+            if (C.N(mid) < q) l = mid + 1;
+            else h = mid;
+        }
+        if (l < end && C.N(l) == q) {
+            const uint32_t k = atomicAdd(&sh.dag_cnt, 1u);
+            if (k < kBT) {
+                sh.cbase[k] = l;
+                sh.cslot[k] = q;
+                sh.scan[k] = m;
+                sh.cval[k] = S.sigma(sl);
+            }
+        }
+    }
+    const uint32_t wp = __reduce_add_sync(kFull, probes);
+    if (C.lane == 0 && wp) atomicAdd(&sh.st_back, static_cast<unsigned long long>(wp));
+    __syncthreads();
+    const uint32_t c = sh.dag_cnt;
+    if (c == 0 || c > kBT) {
+        __syncthreads();
+        return false;
+    }
+    const bool mine = C.tid < c;
+    const uint32_t my_pos = mine ? sh.cbase[C.tid] : 0u;
+    const unsigned long long my_sig = mine ? sh.cval[C.tid] : 0ull;
+    unsigned long long pre_lo = 0;
+    uint32_t pre_hi = 0;
+    if (mine)
+        for (uint32_t j = 0; j < c; ++j)
+            if (sh.cbase[j] < my_pos) add65(pre_lo, pre_hi, sh.cval[j], 0u);
+    // candidate intervals [pre, pre + sigma) in scan order are disjoint: at most one holds r
+    const bool hit = mine && pre_hi == 0 && pre_lo <= r && r - pre_lo < my_sig;
+    if (C.tid == 0) sh.first = kNone;
+    __syncthreads();
+    if (hit) {
+        sh.first = C.tid;
+        sh.bch = sh.cslot[C.tid];
+        sh.bchm = sh.scan[C.tid];
+        sh.bchs = my_sig;
+    }
+    __syncthreads();
+    const bool ok = sh.first != kNone;
+    if (ok) {
+        cur = sh.bch;
+        cmeta = sh.bchm;
+        csig = sh.bchs;
+    }
+    __syncthreads();
+    return ok;
+}
+
 template <int kMode, class Store>
 __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t t, Meet mt,
                           uint32_t frame_local) {
@@ -1017,6 +1105,15 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             __syncthreads();
             if (!found) return false;
         }
+#if ADSB_LEVEL_PICK
+        if (!found && end - beg > 2 * kBT) {
+            const uint32_t lo = want_t ? S.tlev[want_dist] : S.slev[want_dist];
+            const uint32_t hi = want_t ? S.tlev[want_dist + 1] : S.slev[want_dist + 1];
+            const uint32_t deg = end - beg;
+            if (hi - lo <= 4 * kBT && 2ull * (hi - lo) * (32 - __clz(deg)) < deg)
+                found = level_pick(C, S, beg, end, lo, hi, want_t, want_dist, r, cur, cmeta, csig);
+        }
+#endif
         // the next round's neighbour id is loaded one round ahead, so its
         // latency overlaps this round's barriers (hub steps take many rounds)
         uint32_t q_next = !found && beg + C.tid < end ? C.N(beg + C.tid) : 0u;
@@ -1196,6 +1293,7 @@ __device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Sha
     sm.qcap = H / 2;
     sm.qv = sm.km + H;                                     // H/2 x u32
     sm.tlev = sh.tlev_small;
+    sm.slev = sh.slev_small;
     sm.cap = H;
     sm.limit = H / 2;
     sm.level_cap = kSmemLevels;
@@ -1209,6 +1307,7 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
+    gs.slev = p.tlev + static_cast<size_t>(p.level_cap) * (p.slots + slot);
     gs.dq = p.dagq + static_cast<size_t>(p.slot_stride) * slot;
     gs.clear = p.clear_layout != 0;
     gs.tag = tag;
