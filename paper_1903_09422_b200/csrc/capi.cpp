@@ -137,7 +137,28 @@ adsb_status adsb_graph_from_csr(uint32_t n, const uint64_t* offsets, const uint3
         need(out, "out");
         need(offsets, "offsets");
         if (offsets[n]) need(neighbors, "neighbors");
-        *out = wrap(graph_from_csr(n, offsets, neighbors));
+        // With a GPU present, the current device's CSR replica is uploaded
+        // range by range while the host copy is still being validated.
+        int count = 0;
+        if (std::getenv("ADSB_NO_EAGER_UPLOAD") || cudaGetDeviceCount(&count) != cudaSuccess || count == 0 ||
+            offsets[n] >= 0xFFFFFFFFull) {
+            cudaGetLastError();
+            *out = wrap(graph_from_csr(n, offsets, neighbors));
+            return;
+        }
+        const int dev = resolve_device(-1);
+        auto up = begin_streaming_upload(n, offsets[n], dev);
+        HostGraph h;
+        try {
+            h = graph_from_csr(n, offsets, neighbors, streaming_sink(*up));
+        } catch (...) {
+            abort_streaming_upload(std::move(up));
+            throw;
+        }
+        auto ctx = finish_streaming_upload(std::move(up), h);
+        adsb_graph* g = wrap(std::move(h));
+        g->devices.emplace(dev, std::move(ctx));
+        *out = g;
     });
 }
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -179,6 +180,20 @@ struct DeviceContext {
 
 int resolve_device(int requested);
 std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int device);
+// Streaming construction (adsb_graph_from_csr): device buffers are taken
+// first and each validated host range is uploaded as soon as its worker is
+// done, so the copy overlaps validation of the other ranges.
+struct StreamingUpload : CsrChunkSink {
+    std::unique_ptr<DeviceContext> ctx;
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> off32;  // u32 offsets staging (page-locked when large)
+    std::atomic<uint32_t> max_degree{0};
+    std::unique_lock<std::mutex> lock;  // the device runtime (its stream) while uploading
+    void chunk(uint64_t b, uint64_t e, uint64_t nb, uint64_t ne, const HostGraph& g) override;
+};
+std::unique_ptr<StreamingUpload> begin_streaming_upload(uint32_t n, uint64_t nnz, int device);
+inline CsrChunkSink* streaming_sink(StreamingUpload& up) { return &up; }
+std::unique_ptr<DeviceContext> finish_streaming_upload(std::unique_ptr<StreamingUpload> up, const HostGraph& g);
+void abort_streaming_upload(std::unique_ptr<StreamingUpload> up);
 
 // graph.hpp:153-175 connected_components: labels numbered by smallest member
 // (exactly the reference's numbering); returns the component count.

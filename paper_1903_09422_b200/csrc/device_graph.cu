@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 
@@ -328,6 +329,59 @@ std::unique_ptr<DeviceContext> make_device_context(const HostGraph& g, int devic
                                   cudaMemcpyHostToDevice, ctx->rt->stream));
     ADSB_CUDA(cudaStreamSynchronize(ctx->rt->stream));
     return ctx;
+}
+
+void StreamingUpload::chunk(uint64_t b, uint64_t e, uint64_t nb, uint64_t ne, const HostGraph& g) {
+    uint32_t md = 0;
+    for (uint64_t u = b; u < e; ++u) {
+        off32[u] = static_cast<uint32_t>(g.offsets[u]);
+        if (u + 1 < e) md = std::max<uint32_t>(md, static_cast<uint32_t>(g.offsets[u + 1] - g.offsets[u]));
+    }
+    // the range's last vertex ends where the range's adjacency ends
+    if (e > b) md = std::max<uint32_t>(md, static_cast<uint32_t>(ne - g.offsets[e - 1]));
+    uint32_t cur = max_degree.load();
+    while (md > cur && !max_degree.compare_exchange_weak(cur, md)) {
+    }
+    DeviceGraph& dg = ctx->graph;
+    ADSB_CUDA(cudaMemcpyAsync(dg.offsets.ptr + b, off32.data() + b, (e - b) * sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, ctx->rt->stream));
+    if (ne > nb)
+        ADSB_CUDA(cudaMemcpyAsync(dg.nbrs.ptr + nb, g.nbrs.data() + nb, (ne - nb) * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, ctx->rt->stream));
+}
+
+std::unique_ptr<StreamingUpload> begin_streaming_upload(uint32_t n, uint64_t nnz, int device) {
+    if (nnz >= 0xFFFFFFFFull) invalid("device CSR needs fewer than 2^32 adjacency entries");
+    ADSB_CUDA(cudaSetDevice(device));
+    auto up = std::make_unique<StreamingUpload>();
+    up->ctx = std::make_unique<DeviceContext>();
+    DeviceContext& ctx = *up->ctx;
+    ctx.device = device;
+    ctx.rt = &device_runtime(device);
+    up->lock = std::unique_lock<std::mutex>(ctx.rt->mu);
+    ctx.graph.device = device;
+    ctx.graph.n = n;
+    ctx.graph.nnz = nnz;
+    up->off32.resize(static_cast<size_t>(n) + 1);
+    ctx.graph.offsets = take_buffer(*ctx.rt, static_cast<size_t>(n) + 1);
+    ctx.graph.nbrs = take_buffer(*ctx.rt, std::max<uint64_t>(1, nnz));
+    ctx.labels = take_buffer(*ctx.rt, std::max<uint32_t>(1, n));
+    return up;
+}
+
+std::unique_ptr<DeviceContext> finish_streaming_upload(std::unique_ptr<StreamingUpload> up, const HostGraph& g) {
+    DeviceContext& ctx = *up->ctx;
+    up->off32[g.n] = static_cast<uint32_t>(g.offsets[g.n]);
+    ADSB_CUDA(cudaMemcpyAsync(ctx.graph.offsets.ptr + g.n, up->off32.data() + g.n, sizeof(uint32_t),
+                              cudaMemcpyHostToDevice, ctx.rt->stream));
+    ctx.graph.max_degree = up->max_degree.load();
+    // off32 is released below: the copies from it must have landed
+    ADSB_CUDA(cudaStreamSynchronize(ctx.rt->stream));
+    return std::move(up->ctx);
+}
+
+void abort_streaming_upload(std::unique_ptr<StreamingUpload> up) {
+    if (up && up->ctx && up->ctx->rt) cudaStreamSynchronize(up->ctx->rt->stream);
 }
 
 static unsigned grid_for(uint64_t work, int device, unsigned block = 256) {

@@ -216,6 +216,10 @@ HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
 }
 
 HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs) {
+    return graph_from_csr(n, offsets, nbrs, nullptr);
+}
+
+HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs, CsrChunkSink* sink) {
     if (offsets[0] != 0) invalid("offsets[0] must be 0");
     for (uint32_t u = 0; u < n; ++u)
         if (offsets[u + 1] < offsets[u]) invalid("offsets must be non-decreasing");
@@ -239,6 +243,7 @@ HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nb
             }
         }
         if (local_bad) bad = true;
+        else if (sink) sink->chunk(b, e, offsets[b], offsets[e], g);
     });
     g.offsets[n] = offsets[n];
     if (bad) invalid("CSR must have in-range, ascending, duplicate-free, loop-free adjacency");

@@ -70,6 +70,16 @@ struct HostGraph {
 
 HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m);
 HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs);
+// The same, calling chunk(b, e, g) from the worker that has just copied and
+// validated vertices [b, e) into g (the device upload of that range can start
+// while other ranges are still being validated). Throws after all workers
+// finished if any range was invalid.
+struct CsrChunkSink {
+    // vertices [b, e), adjacency entries [nb, ne) of g
+    virtual void chunk(uint64_t b, uint64_t e, uint64_t nb, uint64_t ne, const HostGraph& g) = 0;
+    virtual ~CsrChunkSink() = default;
+};
+HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs, CsrChunkSink* sink);
 HostGraph parse_edge_list_text(const char* text, uint64_t len);
 HostGraph parse_edge_list_file(const std::string& path);
 HostGraph graph_from_pairs(const uint64_t* pairs, uint64_t m);

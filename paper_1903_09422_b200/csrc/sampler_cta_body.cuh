@@ -234,6 +234,9 @@ struct SmemStore {
 //    push rebuild; on C3/C5 the blind CAS and one-pass sums cost 15-35%
 //    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
+#ifndef ADSB_FALLBACK_FILTER
+#define ADSB_FALLBACK_FILTER 1
+#endif
 #ifndef ADSB_LEVEL_PICK
 #define ADSB_LEVEL_PICK 1
 #endif
@@ -257,6 +260,25 @@ struct GlobalStoreT {
     uint32_t qcap;
     uint32_t level_cap;
     bool clear;        // cleared layout (see above)
+    // Fallback samples of the shared-memory kernels: a membership filter of
+    // the claimed vertices (2^18 bits, one hash) in the idle table memory. A
+    // clear bit proves "not claimed", so probes skip the global load, and
+    // levels probe before they claim (room_for is false) as with the table:
+    // the meeting level, the biggest, then claims nothing.
+    uint32_t* filt;
+    static constexpr uint32_t kFiltLog = 18;
+    __device__ static uint32_t fhash(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - kFiltLog); }
+    __device__ void fset(uint32_t v) {
+        if (filt) {
+            const uint32_t h = fhash(v);
+            atomicOr(filt + (h >> 5), 1u << (h & 31));
+        }
+    }
+    __device__ bool fmiss(uint32_t v) const {
+        if (!filt) return false;
+        const uint32_t h = fhash(v);
+        return !(filt[h >> 5] & (1u << (h & 31)));
+    }
 
     __device__ void begin(uint32_t) {}
     // Cleared layout: zero the state of every vertex this sample claimed
@@ -275,6 +297,7 @@ struct GlobalStoreT {
         }
     }
     __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
+        if (fmiss(v)) return kNone;
         const unsigned long long x = __ldcg(st + 2ull * v);
         if (clear ? x == 0ull : static_cast<uint32_t>(x >> 32) != tag) return kNone;
         meta = static_cast<uint32_t>(x);
@@ -287,6 +310,7 @@ struct GlobalStoreT {
             const unsigned long long prev = atomicCAS(st + 2ull * v, 0ull, kPresent | new_meta);
             inserted = prev == 0ull;
             meta = inserted ? new_meta : static_cast<uint32_t>(prev);
+            if (inserted) fset(v);
             return v;
         }
         unsigned long long x = __ldcg(st + 2ull * v);
@@ -296,6 +320,7 @@ struct GlobalStoreT {
             if (prev == x) {
                 inserted = true;
                 meta = new_meta;
+                fset(v);
                 return v;
             }
             x = prev;
@@ -315,6 +340,7 @@ struct GlobalStoreT {
         if (tok == ~0ull) return claim<kReserve>(v, new_meta, inserted, meta);
         inserted = tok == 0ull;
         meta = inserted ? new_meta : static_cast<uint32_t>(tok);
+        if (inserted) fset(v);
         return v;
     }
     // sigma is zero before the claim, so claims and sums share one pass
@@ -333,7 +359,7 @@ struct GlobalStoreT {
     __device__ unsigned long long sigma(uint32_t slot) const { return __ldcg(st + 2ull * slot + 1); }
     __device__ bool queue_ok(uint32_t, uint32_t) const { return true; }
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
-    __device__ bool room_for(unsigned long long) const { return true; }
+    __device__ bool room_for(unsigned long long) const { return filt == nullptr; }
     __device__ void set_level(uint32_t*, uint32_t) {}
 };
 
@@ -1310,6 +1336,7 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const
     gs.slev = p.tlev + static_cast<size_t>(p.level_cap) * (p.slots + slot);
     gs.dq = p.dagq + static_cast<size_t>(p.slot_stride) * slot;
     gs.clear = p.clear_layout != 0;
+    gs.filt = nullptr;
     gs.tag = tag;
     gs.qcap = p.n;
     gs.level_cap = p.level_cap;
@@ -1382,10 +1409,23 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             tag = sh.g_tag;
         }
         auto gs = make_global_store(p, region, tag);
+#if ADSB_FALLBACK_FILTER
+        // the table is empty here (the overflowed attempt cleared it) and
+        // covers the filter: 2^18 bits = 32 KB <= hash_cap * 12 B
+        if constexpr (!kGlobalOnly)
+            if (p.hash_cap * 12u >= (1u << GlobalStoreT<ADSB_LOAD_BATCH>::kFiltLog) / 8u)
+                gs.filt = reinterpret_cast<uint32_t*>(adsb_dyn);
+#endif
         rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
         if constexpr (!kGlobalOnly) {
             __syncthreads();  // every thread is done with the region
             if (C.tid == 0) release_region(p, region, tag);
+#if ADSB_FALLBACK_FILTER
+            if (gs.filt) {
+                make_smem_store(p, *C.sh).clear_all(C.tid);  // the next sample needs an empty table
+                __syncthreads();
+            }
+#endif
         }
     }
     if (rc != 0 && C.tid == 0) C.sh->n_errors += 1;
