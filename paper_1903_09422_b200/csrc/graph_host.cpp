@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -106,6 +108,74 @@ void host_block_free(void* p, size_t bytes) noexcept {
     cudaGetLastError();
 }
 
+// Persistent host workers: spawning a std::thread per range cost ~40 us each
+// (0.6 ms of C2's 1.75 ms graph_from_csr on 16 cores). run(T, f) calls f(i)
+// for i in [0, T): i = 0 on the caller, the rest on pool workers. Calls are
+// serialised; a call from inside a worker runs inline.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool* pool = new HostPool();  // never destroyed (workers detach at exit)
+        return *pool;
+    }
+    void run(unsigned T, const std::function<void(unsigned)>& f) {
+        if (T <= 1 || in_worker()) {
+            for (unsigned i = 0; i < T; ++i) f(i);
+            return;
+        }
+        std::lock_guard<std::mutex> serial(run_mu_);
+        ensure(T - 1);
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            job_ = &f;
+            active_ = T - 1;
+            pending_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0);
+        std::unique_lock<std::mutex> lock(mu_);
+        done_cv_.wait(lock, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    static bool& in_worker() {
+        static thread_local bool w = false;
+        return w;
+    }
+    void ensure(unsigned workers) {
+        while (threads_.size() < workers) {
+            const unsigned id = static_cast<unsigned>(threads_.size());
+            threads_.emplace_back([this, id] { loop(id); });
+            threads_.back().detach();
+        }
+    }
+    void loop(unsigned id) {
+        in_worker() = true;
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(unsigned)>* job;
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                cv_.wait(lock, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (id >= active_) continue;
+                job = job_;
+            }
+            (*job)(id + 1);
+            std::lock_guard<std::mutex> lock(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> threads_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    unsigned active_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+};
+
 template <class F>
 static void parallel_for(uint64_t count, F&& body) {
     const unsigned T = host_threads();
@@ -113,14 +183,11 @@ static void parallel_for(uint64_t count, F&& body) {
         body(0, count);
         return;
     }
-    std::vector<std::thread> th;
     const uint64_t chunk = (count + T - 1) / T;
-    for (unsigned t = 0; t < T; ++t) {
+    HostPool::get().run(T, [&](unsigned t) {
         const uint64_t b = t * chunk, e = std::min(count, b + chunk);
-        if (b >= e) break;
-        th.emplace_back([&, b, e] { body(b, e); });
-    }
-    for (auto& x : th) x.join();
+        if (b < e) body(b, e);
+    });
 }
 
 // parallel_for over vertices [0, n) with ranges of about equal adjacency
@@ -133,7 +200,7 @@ static void parallel_for_weighted(uint64_t n, const uint64_t* offsets, F&& body)
         body(0, n);
         return;
     }
-    std::vector<std::thread> th;
+    std::vector<uint64_t> cut(1, 0);
     uint64_t b = 0;
     for (unsigned t = 0; t < T && b < n; ++t) {
         uint64_t e = n;
@@ -147,10 +214,10 @@ static void parallel_for_weighted(uint64_t n, const uint64_t* offsets, F&& body)
             }
             e = std::max(lo, b + 1);
         }
-        th.emplace_back([&, b, e] { body(b, e); });
+        cut.push_back(e);
         b = e;
     }
-    for (auto& x : th) x.join();
+    HostPool::get().run(static_cast<unsigned>(cut.size() - 1), [&](unsigned t) { body(cut[t], cut[t + 1]); });
 }
 
 
@@ -382,10 +449,7 @@ HostGraph parse_edge_list_text(const char* text, uint64_t len) {
     if (T == 1) {
         parse_chunk(text, text + len, parts[0]);
     } else {
-        std::vector<std::thread> th;
-        for (unsigned t = 0; t < T; ++t)
-            th.emplace_back([&, t] { parse_chunk(text + cut[t], text + cut[t + 1], parts[t]); });
-        for (auto& x : th) x.join();
+        HostPool::get().run(T, [&](unsigned t) { parse_chunk(text + cut[t], text + cut[t + 1], parts[t]); });
     }
     uint64_t lines_before = 0, total = 0;
     for (const ChunkParse& r : parts) {

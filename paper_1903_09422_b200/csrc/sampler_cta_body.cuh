@@ -234,6 +234,9 @@ struct SmemStore {
 //    push rebuild; on C3/C5 the blind CAS and one-pass sums cost 15-35%
 //    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
+#ifndef ADSB_PF_DIST
+#define ADSB_PF_DIST 1  // adjacency prefetch distance (rounds of kBT edges) in for_edges
+#endif
 #ifndef ADSB_FALLBACK_FILTER
 #define ADSB_FALLBACK_FILTER 1
 #endif
@@ -559,8 +562,8 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                     vv[k] = C.N(o_base + e);
                     // pull this thread's next adjacency id into L1 while the
                     // body runs (same row: the common case inside hub lists)
-                    if (k + 1 == kBatch && e + kBT < o_end)
-                        asm volatile("prefetch.global.L1 [%0];" ::"l"(C.nbrs + o_base + e + kBT));
+                    if (k + 1 == kBatch && e + ADSB_PF_DIST * kBT < o_end)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(C.nbrs + o_base + e + ADSB_PF_DIST * kBT));
                     owners |= ow << (8 * k);
                     cnt = k + 1;
                 }
