@@ -289,6 +289,8 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     // Low-degree graphs (cleared layout): 3 blocks per SM beat 4 (C4 -4%:
     // fewer concurrent samples keep more of their frontier state in L2).
     if (a.layout == 1) p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * 3);
+    p.global_threads = 256;
+    if (const char* e = std::getenv("ADSB_GLOBAL_BT")) p.global_threads = std::strtoul(e, nullptr, 10) == 512 ? 512 : 256;
     if (const char* e = std::getenv("ADSB_GLOBAL_GRID")) p.global_grid = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     p.block_threads = a.block_threads;
     return p;

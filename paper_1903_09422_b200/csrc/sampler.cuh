@@ -57,6 +57,7 @@ struct SamplerParams {
     uint32_t use_smem;     // block sampler: try the shared-memory store first
     uint32_t block_threads; // block sampler: 128 or 256
     uint32_t global_grid;   // block sampler: resident blocks of the global-store-only variant
+    uint32_t global_threads; // block sampler: threads per block of the global-store-only variant (256 or 512)
     uint32_t max_degree;    // graph max degree (low-degree graphs use thread-per-vertex expansion)
     uint32_t clear_layout;  // block teams: global state in the cleared layout (else tagged)
     float csr_hint;         // block teams: fraction of CSR reads marked L2 evict_last (1 when the CSR fits L2/2)

@@ -94,6 +94,14 @@ constexpr int kBT = 256;
 #include "sampler_cta_body.cuh"
 }  // namespace bt256
 
+// 512-thread teams for the global-store-only kernel (low-degree graphs:
+// half the samples in flight for the same threads, so more of each
+// sample's frontier state stays in L2)
+namespace bt512 {
+constexpr int kBT = 512;
+#include "sampler_cta_body.cuh"
+}  // namespace bt512
+
 size_t sampler_cta_smem_bytes(uint32_t hash_cap) {
     return static_cast<size_t>(hash_cap) * 12 + static_cast<size_t>(hash_cap / 2) * 4;  // sigma, key|meta, queue
 }
@@ -115,6 +123,9 @@ void configure_once() {
     allow_big_smem(bt256::sampler_cta_kernel<kModeDet, true>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, true>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeFused, true>);
+    allow_big_smem(bt512::sampler_cta_kernel<kModeDet, true>);
+    allow_big_smem(bt512::sampler_cta_kernel<kModeEpoch, true>);
+    allow_big_smem(bt512::sampler_cta_kernel<kModeFused, true>);
     done = true;
 }
 }  // namespace
@@ -144,7 +155,10 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
     if (!p.use_smem) {
         const unsigned grid = std::min<unsigned>(p.slots, p.global_grid);
-        if (deterministic) bt256::sampler_cta_kernel<kModeDet, true><<<grid, 256, 0, stream>>>(p);
+        if (p.global_threads == 512) {
+            if (deterministic) bt512::sampler_cta_kernel<kModeDet, true><<<grid, 512, 0, stream>>>(p);
+            else bt512::sampler_cta_kernel<kModeEpoch, true><<<grid, 512, 0, stream>>>(p);
+        } else if (deterministic) bt256::sampler_cta_kernel<kModeDet, true><<<grid, 256, 0, stream>>>(p);
         else bt256::sampler_cta_kernel<kModeEpoch, true><<<grid, 256, 0, stream>>>(p);
         ADSB_CUDA(cudaGetLastError());
         return;
@@ -163,7 +177,10 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     configure_once();
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
     if (!p.use_smem) {
-        bt256::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 256, 0, stream>>>(p);
+        if (p.global_threads == 512)
+            bt512::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 512, 0, stream>>>(p);
+        else
+            bt256::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 256, 0, stream>>>(p);
         ADSB_CUDA(cudaGetLastError());
         return;
     }

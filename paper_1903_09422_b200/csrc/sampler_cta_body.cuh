@@ -539,7 +539,8 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         // staging through shared memory would wait on each load in turn).
         // Owner indices pack into one register (8 bits each).
         constexpr uint32_t kBatch = Store::kLoadBatch;
-        static_assert(kBT <= 256 && kBatch <= 4, "owner indices pack into 32 bits");
+        constexpr uint32_t kOwnerBits = kBT <= 256 ? 8 : 16;
+        static_assert(kBT <= 65536 && kBatch * kOwnerBits <= 32, "owner indices pack into 32 bits");
         for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kBatch) {
             uint32_t owners = 0, cnt = 0;
             uint32_t vv[kBatch];
@@ -564,7 +565,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                     // body runs (same row: the common case inside hub lists)
                     if (k + 1 == kBatch && e + ADSB_PF_DIST * kBT < o_end)
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(C.nbrs + o_base + e + ADSB_PF_DIST * kBT));
-                    owners |= ow << (8 * k);
+                    owners |= ow << (kOwnerBits * k);
                     cnt = k + 1;
                 }
             }
@@ -572,8 +573,8 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             for (uint32_t k = 0; k < cnt; ++k) {
                 const uint32_t v = vv[0];
                 ADSB_DCHECK(v < C.n);
-                const uint32_t w = owners & 0xFFu;
-                owners >>= 8;
+                const uint32_t w = owners & ((1u << kOwnerBits) - 1u);
+                owners >>= kOwnerBits;
                 body(sh.cslot[w], sh.cval[w], v, kNoTok);
 #pragma unroll
                 for (uint32_t j = 0; j + 1 < kBatch; ++j) vv[j] = vv[j + 1];
@@ -1528,7 +1529,7 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
 }
 
 template <int kMode, bool kGlobalOnly>
-__global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB : ADSB_MINB_PER_256 * 256 / kBT)
+__global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kBT : ADSB_MINB_PER_256 * 256 / kBT)
     sampler_cta_kernel(SamplerParams p) {
     __shared__ Shared sh;
     Ctx C;
