@@ -286,11 +286,19 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.hash_cap = a.hash_cap;
     p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
     p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
-    // Low-degree graphs (cleared layout): 3 blocks per SM beat 4 (C4 -4%:
-    // fewer concurrent samples keep more of their frontier state in L2).
-    if (a.layout == 1) p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * 3);
+    // Low-degree graphs (cleared layout): fewer, wider teams. Half the samples
+    // in flight for the same threads keeps more of each sample's frontier
+    // state in L2: 2 blocks of 512 per SM beat 3 of 256 (C4 -19%), which beat
+    // 4 of 256 (-4%); profiles/r01_ab_round3.txt.
     p.global_threads = 256;
-    if (const char* e = std::getenv("ADSB_GLOBAL_BT")) p.global_threads = std::strtoul(e, nullptr, 10) == 512 ? 512 : 256;
+    if (a.layout == 1) {
+        p.global_threads = 512;
+        p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * 2);
+    }
+    if (const char* e = std::getenv("ADSB_GLOBAL_BT")) {
+        const unsigned long bt = std::strtoul(e, nullptr, 10);
+        p.global_threads = bt == 1024 ? 1024 : bt == 512 ? 512 : 256;
+    }
     if (const char* e = std::getenv("ADSB_GLOBAL_GRID")) p.global_grid = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     p.block_threads = a.block_threads;
     return p;

@@ -102,6 +102,11 @@ constexpr int kBT = 512;
 #include "sampler_cta_body.cuh"
 }  // namespace bt512
 
+namespace bt1024 {
+constexpr int kBT = 1024;
+#include "sampler_cta_body.cuh"
+}  // namespace bt1024
+
 size_t sampler_cta_smem_bytes(uint32_t hash_cap) {
     return static_cast<size_t>(hash_cap) * 12 + static_cast<size_t>(hash_cap / 2) * 4;  // sigma, key|meta, queue
 }
@@ -126,6 +131,9 @@ void configure_once() {
     allow_big_smem(bt512::sampler_cta_kernel<kModeDet, true>);
     allow_big_smem(bt512::sampler_cta_kernel<kModeEpoch, true>);
     allow_big_smem(bt512::sampler_cta_kernel<kModeFused, true>);
+    allow_big_smem(bt1024::sampler_cta_kernel<kModeDet, true>);
+    allow_big_smem(bt1024::sampler_cta_kernel<kModeEpoch, true>);
+    allow_big_smem(bt1024::sampler_cta_kernel<kModeFused, true>);
     done = true;
 }
 }  // namespace
@@ -155,7 +163,10 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
     if (!p.use_smem) {
         const unsigned grid = std::min<unsigned>(p.slots, p.global_grid);
-        if (p.global_threads == 512) {
+        if (p.global_threads == 1024) {
+            if (deterministic) bt1024::sampler_cta_kernel<kModeDet, true><<<grid, 1024, 0, stream>>>(p);
+            else bt1024::sampler_cta_kernel<kModeEpoch, true><<<grid, 1024, 0, stream>>>(p);
+        } else if (p.global_threads == 512) {
             if (deterministic) bt512::sampler_cta_kernel<kModeDet, true><<<grid, 512, 0, stream>>>(p);
             else bt512::sampler_cta_kernel<kModeEpoch, true><<<grid, 512, 0, stream>>>(p);
         } else if (deterministic) bt256::sampler_cta_kernel<kModeDet, true><<<grid, 256, 0, stream>>>(p);
@@ -177,7 +188,9 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     configure_once();
     const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
     if (!p.use_smem) {
-        if (p.global_threads == 512)
+        if (p.global_threads == 1024)
+            bt1024::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 1024, 0, stream>>>(p);
+        else if (p.global_threads == 512)
             bt512::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 512, 0, stream>>>(p);
         else
             bt256::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 256, 0, stream>>>(p);

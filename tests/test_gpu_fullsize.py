@@ -16,7 +16,9 @@ checked through size-independent properties:
   frames equal the oracle's;
 * a deep, low-degree lattice with holes (C4's shape, smaller): sampled paths
   equal the oracle's on the global-state store with thread-per-vertex
-  expansion.
+  expansion (C4 itself: test_gpu_parity.py::test_degenerate_sigma_frames_c4);
+* C5 at full size: paths identical with and without the shared-memory table,
+  and the fused epoch run reproducible run to run.
 """
 import numpy as np
 import pytest
@@ -135,3 +137,34 @@ def test_holey_lattice_lowdegree_frames(mode, monkeypatch):
     o = oracle.estimate_bc(og, 0.02, 0.1, spf=1, seed=11, nominal_threads=8, max_frames=500)
     assert (r.tau, r.run.check_cycles) == (o.tau, o.check_cycles)
     np.testing.assert_array_equal(r.run.data, o.counts)
+
+
+@pytest.fixture(scope="module")
+def c5_csr():
+    g = datasets.graph("c5_rmat24").graph
+    return g.num_vertices(), np.ascontiguousarray(g.offsets()), np.ascontiguousarray(g.neighbor_list())
+
+
+def test_c5_fullsize_store_invariance_and_reproducibility(c5_csr, monkeypatch):
+    """C5 at full size (8.9M vertices, 2.1 GB CSR): sampled paths are the same
+    with the shared-memory table (+ global fallback with the membership filter)
+    and with the global store alone; the fused cumulative-epoch run is
+    reproducible run to run (epochs are index ranges)."""
+    n, off, nb = c5_csr
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    g1 = adsamp.Graph.from_csr(n, off, nb)
+    a = sample_frames(g1, 42, 1, 0, 400, device=0)
+    monkeypatch.setenv("ADSB_NO_SMEM", "1")
+    g2 = adsamp.Graph.from_csr(n, off, nb)
+    b = sample_frames(g2, 42, 1, 0, 400, device=0)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    assert sum(len(x) for x in a) > 400
+    monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
+    w = datasets.CONFIGS["c5_rmat24"]
+    cfg = EngineConfig(variant=Variant.shared, threads=8, base_seed=42, device=0, max_cycles=48)
+    r1 = estimate_bc(g1, w.epsilon, w.delta, cfg)
+    r2 = estimate_bc(g1, w.epsilon, w.delta, cfg)
+    assert r1.tau == r2.tau == 48 * 1024 and r1.reason.name == "capped"
+    np.testing.assert_array_equal(r1.run.data, r2.run.data)
