@@ -329,12 +329,15 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
         // r.counts points into the runtime's pinned buffer: copied out while the
         // runtime lock (L) is still held
         if (counts) {
-            if (r.counts) std::copy(r.counts, r.counts + n, counts);
+            if (r.counts)  // fresh caller memory: page faults and widening spread over the host workers
+                host_parallel_for(n, [&](uint64_t b, uint64_t e) { std::copy(r.counts + b, r.counts + e, counts + b); });
             else std::fill(counts, counts + n, uint64_t{0});
         }
         if (scores)  // kadabra.hpp:334-337
-            for (uint32_t v = 0; v < n; ++v)
-                scores[v] = r.tau == 0 || !r.counts ? 0.0 : static_cast<double>(r.counts[v]) / static_cast<double>(r.tau);
+            host_parallel_for(n, [&](uint64_t b, uint64_t e) {
+                for (uint64_t v = b; v < e; ++v)
+                    scores[v] = r.tau == 0 || !r.counts ? 0.0 : static_cast<double>(r.counts[v]) / static_cast<double>(r.tau);
+            });
         if (stats) {
             stats->tau = r.tau;
             stats->check_cycles = r.check_cycles;

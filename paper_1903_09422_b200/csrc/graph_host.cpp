@@ -190,6 +190,10 @@ static void parallel_for(uint64_t count, F&& body) {
     });
 }
 
+void host_parallel_for(uint64_t count, const std::function<void(uint64_t, uint64_t)>& body) {
+    parallel_for(count, body);
+}
+
 // parallel_for over vertices [0, n) with ranges of about equal adjacency
 // volume (offsets: n+1 prefix sums).
 template <class F>

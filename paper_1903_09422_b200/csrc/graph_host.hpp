@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <utility>
@@ -67,6 +68,9 @@ struct HostGraph {
     uint64_t nnz() const { return nbrs.size(); }
     uint64_t degree(uint32_t u) const { return offsets[u + 1] - offsets[u]; }
 };
+
+// [0, count) split over the persistent host workers (inline when small)
+void host_parallel_for(uint64_t count, const std::function<void(uint64_t, uint64_t)>& body);
 
 HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m);
 HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs);
