@@ -234,6 +234,9 @@ struct SmemStore {
 //    push rebuild; on C3/C5 the blind CAS and one-pass sums cost 15-35%
 //    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
+#ifndef ADSB_BT_PREFETCH
+#define ADSB_BT_PREFETCH 1  // backtrack: prefetch the candidates' offsets into L1
+#endif
 #ifndef ADSB_PF_DIST
 #define ADSB_PF_DIST 1  // adjacency prefetch distance (rounds of kBT edges) in for_edges
 #endif
@@ -1096,7 +1099,14 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                         const uint32_t sl = S.find(q, m);
                         cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist &&
                                (!want_t || (m & kMetaDag));
-                        if (cand) val = S.sigma(sl);
+                        if (cand) {
+                            val = S.sigma(sl);
+#if ADSB_BT_PREFETCH
+                            // one of the candidates is the next step's cur: its offsets
+                            // line is in L1 when that step starts
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(C.off + q));
+#endif
+                        }
                     }
                     if (C.lane == 0) sh.st_back += min(32u, end - base);
                     const uint32_t cb = __ballot_sync(kFull, cand);
@@ -1154,8 +1164,12 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             if (i + kBT < end) q_next = C.N(i + kBT);
             if (i < end) {
                 const uint32_t sl = S.find(q, m);
-                if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag)))
+                if (sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist && (!want_t || (m & kMetaDag))) {
                     val = S.sigma(sl);
+#if ADSB_BT_PREFETCH
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(C.off + q));
+#endif
+                }
             }
             if (C.tid == 0) sh.st_back += min(static_cast<uint32_t>(kBT), end - base);
             // per-warp 65-bit candidate totals, then the warp whose range holds
