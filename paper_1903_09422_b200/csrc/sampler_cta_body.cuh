@@ -235,7 +235,7 @@ struct SmemStore {
 //    (same-address atomics on hubs, sums on the meeting level).
 // kU: adjacency loads kept in flight per thread by for_edges.
 #ifndef ADSB_BT_PREFETCH
-#define ADSB_BT_PREFETCH 1  // backtrack: prefetch the candidates' offsets into L1
+#define ADSB_BT_PREFETCH 0  // backtrack: prefetch the candidates offsets into L1 (measured neutral)
 #endif
 #ifndef ADSB_PF_DIST
 #define ADSB_PF_DIST 1  // adjacency prefetch distance (rounds of kBT edges) in for_edges

@@ -286,3 +286,32 @@ def test_block_teams_frames_ba(mode, spf, monkeypatch):
     o = oracle.estimate_bc(og, 0.02, 0.1, spf=spf, seed=21, nominal_threads=4, max_frames=600)
     assert (r.tau, r.run.check_cycles, r.reason.name) == (o.tau, o.check_cycles, o.reason)
     np.testing.assert_array_equal(r.run.data, o.counts)
+
+
+def test_fused_epoch_audit_replay(tmp_path, monkeypatch):
+    """validate_consistency-style replay of the fused epoch pipeline
+    (audit.hpp:101-161 analogue): with ADSB_FUSED_AUDIT the
+    kernel records, per sample, how many increments it made (and its distance),
+    and per epoch how many increments the in-order fold consumed. Every sample
+    of a folded epoch must have recorded exactly its path's interior vertices
+    (the oracle's path for that stream position), every folded epoch must have
+    consumed exactly the sum over its samples, and nothing past the stop epoch
+    may be folded."""
+    monkeypatch.setenv("ADSB_SAMPLER", "block")
+    audit = tmp_path / "audit.bin"
+    monkeypatch.setenv("ADSB_FUSED_AUDIT", str(audit))
+    pairs = datasets.pairs("c1_er")
+    pg, og = both(pairs)
+    B = 256
+    cfg = EngineConfig(variant=Variant.shared, threads=4, base_seed=5, epoch_samples=B, device=0)
+    r = estimate_bc(pg.graph, 0.02, 0.1, cfg)
+    a = np.fromfile(audit, dtype=np.uint32)
+    max_epochs = a.size // (B + 1)
+    per_sample, folded = a[: max_epochs * B], a[max_epochs * B:]
+    stop = r.run.check_cycles  # epochs folded, in order
+    paths = oracle.sample_frames(og, 5, 1, 0, stop * B)
+    rec = per_sample[: stop * B] & 0xFFFF
+    np.testing.assert_array_equal(rec, np.array([len(p) for p in paths], dtype=np.uint32))
+    np.testing.assert_array_equal(folded[:stop], rec.reshape(stop, B).sum(axis=1))
+    assert not folded[stop:].any()
+    assert int(folded[:stop].sum()) == int(r.run.data.sum())
