@@ -422,7 +422,7 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 // claims issue their compare-and-swaps together (ADSB_LOWDEG_BATCH) instead
 // of one dependent round trip per neighbour.
 #ifndef ADSB_LOWDEG_BATCH
-#define ADSB_LOWDEG_BATCH 0
+#define ADSB_LOWDEG_BATCH 1
 #endif
 constexpr unsigned long long kNoTok = ~0ull;
 template <class Store, class Prep, class Issue, class Body>
