@@ -129,6 +129,33 @@ def test_from_edges_and_csr_validation():
         adsamp.Graph.from_csr(3, [0, 2, 2, 2], [2, 1])  # not ascending
 
 
+def test_large_csr_validation_on_host_workers():
+    """from_csr above the parallel threshold runs on the persistent host
+    workers: a valid CSR round-trips, and a defect in any range (one per
+    worker range tried) is reported, repeatedly (the pool is reused)."""
+    pairs = datasets.gen_gnm(60000, 300000, 3)
+    g = adsamp.graph_from_pairs(pairs).graph
+    off, nb = g.offsets().copy(), g.neighbor_list().copy()
+    assert nb.size >= 262144
+    for _ in range(3):
+        h = adsamp.Graph.from_csr(g.num_vertices(), off, nb)
+        np.testing.assert_array_equal(h.offsets(), off)
+        np.testing.assert_array_equal(h.neighbor_list(), nb)
+    n = g.num_vertices()
+    for frac in (0.02, 0.5, 0.97):
+        u = int(np.searchsorted(off, int(frac * nb.size), side="right")) - 1
+        while off[u + 1] - off[u] < 2:
+            u += 1
+        bad = nb.copy()
+        bad[off[u] + 1] = bad[off[u]]  # duplicate neighbour
+        with pytest.raises(InvalidArgument):
+            adsamp.Graph.from_csr(n, off, bad)
+        bad = nb.copy()
+        bad[off[u]] = u  # self loop
+        with pytest.raises(InvalidArgument):
+            adsamp.Graph.from_csr(n, off, bad)
+
+
 def test_serialize_and_renumbering():
     # graph.hpp:140-144 writes dense ids; re-parsing renumbers them by first
     # appearance, so the round trip is NOT the identity in general (the
