@@ -200,6 +200,7 @@ struct SmemStore {
     }
     __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], 0x40u); }
     __device__ void prefetch(uint32_t) const {}
+    static constexpr bool kBatchClaims = false;
     __device__ unsigned long long claim_issue(uint32_t, uint32_t) { return ~0ull; }
     template <bool kReserve = true>
     __device__ uint32_t claim_tok(uint32_t v, uint32_t new_meta, unsigned long long, bool& inserted, uint32_t& meta) {
@@ -252,9 +253,10 @@ struct SmemStore {
 #ifndef ADSB_LOWDEG_COUNT
 #define ADSB_LOWDEG_COUNT 1
 #endif
-template <uint32_t kU>
+template <uint32_t kU, bool kBatch = false>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
+    static constexpr bool kBatchClaims = kBatch;  // global-store-only kernels
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
     static constexpr unsigned long long kPresent = 1ull << 32;
     unsigned long long* st;  // 2 words per vertex: (tag or present << 32 | meta), sigma
@@ -465,23 +467,25 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                 uint32_t vv[4];
 #pragma unroll
                 for (uint32_t k = 0; k < 4; ++k) vv[k] = j0 + k < e ? C.N(j0 + k) : kNone;
-#if ADSB_LOWDEG_BATCH
-                unsigned long long tok[4];
+                // batched claims only in the global-store-only kernels (the
+                // extra registers would spill in the shared-memory kernels)
+                if constexpr (ADSB_LOWDEG_BATCH && Store::kBatchClaims) {
+                    unsigned long long tok[4];
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k) tok[k] = vv[k] != kNone ? issue(vv[k]) : kNoTok;
-                if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
+                    for (uint32_t k = 0; k < 4; ++k) tok[k] = vv[k] != kNone ? issue(vv[k]) : kNoTok;
+                    if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    if (vv[k] != kNone) body(slot, val, vv[k], tok[k]);
-#else
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (vv[k] != kNone) body(slot, val, vv[k], tok[k]);
+                } else {
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    if (vv[k] != kNone) S.prefetch(vv[k]);
-                if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (vv[k] != kNone) S.prefetch(vv[k]);
+                    if (more && j0 == o) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.off + u_next));
 #pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    if (vv[k] != kNone) body(slot, val, vv[k], kNoTok);
-#endif
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (vv[k] != kNone) body(slot, val, vv[k], kNoTok);
+                }
             }
         }
 #else
@@ -913,6 +917,9 @@ __device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
 #ifndef ADSB_PUSH_BATCH
 #define ADSB_PUSH_BATCH 0
 #endif
+#ifndef ADSB_KARY
+#define ADSB_KARY 1
+#endif
 #ifndef ADSB_PUSH_REBUILD
 #define ADSB_PUSH_REBUILD 1
 #endif
@@ -1020,6 +1027,46 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
     if (C.tid == 0) sh.dag_cnt = 0;
     __syncthreads();
     uint32_t probes = 0;
+#if ADSB_KARY
+    if (hi - lo <= 2 * (kBT / 32)) {
+        // short list: one warp per entry, 32-ary search (each round one
+        // coalesced-ish probe per lane narrows the range 32x: ~4 L2 round trips
+        // for a 10^5-entry hub instead of ~17 dependent ones)
+        for (uint32_t j = lo + C.warp; j < hi; j += kBT / 32) {
+            const uint32_t q = S.qv[want_t ? S.tpos(j) : j];
+            uint32_t m;
+            const uint32_t sl = S.find(q, m);
+            if (sl == kNone || m_is_t(m) != want_t || m_dist(m) != want_dist || (want_t && !(m & kMetaDag)))
+                continue;  // warp-uniform
+            uint32_t l = beg, h = end;  // lower bound of q in [l, h)
+            while (h - l > 32) {
+                const uint32_t step = (h - l + 31) / 32;
+                const uint32_t pos = l + C.lane * step;
+                const bool below = pos < h && C.N(pos) < q;
+                const uint32_t cnt = __popc(__ballot_sync(kFull, below));  // probes below q: a prefix
+                probes += C.lane == 0 ? 32 : 0;
+                const uint32_t nl = cnt == 0 ? l : l + (cnt - 1) * step + 1;
+                const uint32_t nh = cnt == 0 ? l : min(h, l + cnt * step);
+                l = nl;
+                h = nh;
+            }
+            const uint32_t pos = l + C.lane;
+            const uint32_t val = pos < h ? C.N(pos) : 0xFFFFFFFFu;
+            const uint32_t cnt = __popc(__ballot_sync(kFull, pos < h && val < q));
+            const bool hit = __any_sync(kFull, pos < h && val == q);
+            probes += C.lane == 0 ? 32 : 0;
+            if (hit && C.lane == 0) {
+                const uint32_t k = atomicAdd(&sh.dag_cnt, 1u);
+                if (k < kBT) {
+                    sh.cbase[k] = l + cnt;
+                    sh.cslot[k] = q;
+                    sh.scan[k] = m;
+                    sh.cval[k] = S.sigma(sl);
+                }
+            }
+        }
+    } else
+#endif
     for (uint32_t j = lo + C.tid; j < hi; j += kBT) {
         const uint32_t q = S.qv[want_t ? S.tpos(j) : j];
         uint32_t m;
@@ -1371,9 +1418,10 @@ __device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Sha
     return sm;
 }
 
-__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH> make_global_store(const SamplerParams& p, uint32_t slot,
+template <bool kGlobalOnly>
+__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly> make_global_store(const SamplerParams& p, uint32_t slot,
                                                                            uint32_t tag) {
-    GlobalStoreT<ADSB_LOAD_BATCH> gs;
+    GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
@@ -1452,7 +1500,7 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             region = sh.g_region;
             tag = sh.g_tag;
         }
-        auto gs = make_global_store(p, region, tag);
+        auto gs = make_global_store<kGlobalOnly>(p, region, tag);
 #if ADSB_FALLBACK_FILTER
         // the table is empty here (the overflowed attempt cleared it) and
         // covers the filter: 2^18 bits = 32 KB <= hash_cap * 12 B
