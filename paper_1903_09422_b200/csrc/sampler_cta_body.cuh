@@ -918,7 +918,7 @@ __device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
 #define ADSB_PUSH_BATCH 0
 #endif
 #ifndef ADSB_KARY
-#define ADSB_KARY 1
+#define ADSB_KARY 0  // measured slower (spills): C2 +2%, C5 +5%
 #endif
 #ifndef ADSB_PUSH_REBUILD
 #define ADSB_PUSH_REBUILD 1
@@ -1045,8 +1045,9 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
                 const bool below = pos < h && C.N(pos) < q;
                 const uint32_t cnt = __popc(__ballot_sync(kFull, below));  // probes below q: a prefix
                 probes += C.lane == 0 ? 32 : 0;
+                // the lower bound lies in (probe cnt-1, probe cnt]: keep probe cnt
                 const uint32_t nl = cnt == 0 ? l : l + (cnt - 1) * step + 1;
-                const uint32_t nh = cnt == 0 ? l : min(h, l + cnt * step);
+                const uint32_t nh = min(h, l + cnt * step + 1);
                 l = nl;
                 h = nh;
             }
