@@ -244,6 +244,9 @@ struct SmemStore {
 #ifndef ADSB_FALLBACK_FILTER
 #define ADSB_FALLBACK_FILTER 1
 #endif
+#ifndef ADSB_LP_MIN_ROUNDS
+#define ADSB_LP_MIN_ROUNDS 2  // level_pick only for steps of more than this many kBT-wide rounds
+#endif
 #ifndef ADSB_LEVEL_PICK
 #define ADSB_LEVEL_PICK 1
 #endif
@@ -1220,7 +1223,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             if (!found) return false;
         }
 #if ADSB_LEVEL_PICK
-        if (!found && end - beg > 2 * kBT) {
+        if (!found && end - beg > ADSB_LP_MIN_ROUNDS * kBT) {
             const uint32_t lo = want_t ? S.tlev[want_dist] : S.slev[want_dist];
             const uint32_t hi = want_t ? S.tlev[want_dist + 1] : S.slev[want_dist + 1];
             const uint32_t deg = end - beg;
@@ -1678,15 +1681,20 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
                 sh.pending = 0;
                 unsigned long long i = ~0ull;
                 if (!completed) {
+                    // the ticket and both control words are fetched together
+                    // (three round trips in flight, not one after another)
                     i = atomicAdd(p.ctl + kCtlTicket, 1ull);
+                    unsigned long long stop_v = vload(p.ctl + kCtlStop), fold_v = vload(p.ctl + kCtlFolded);
                     const unsigned long long e = i / p.epoch_b;
                     for (;;) {
-                        if (e > vload(p.ctl + kCtlStop) || e >= p.max_epochs) {
+                        if (e > stop_v || e >= p.max_epochs) {
                             i = ~0ull;
                             break;
                         }
-                        if (e < vload(p.ctl + kCtlFolded) + p.ring_k) break;
+                        if (e < fold_v + p.ring_k) break;
                         __nanosleep(200);
+                        stop_v = vload(p.ctl + kCtlStop);
+                        fold_v = vload(p.ctl + kCtlFolded);
                     }
                 }
                 sh.tick[par] = i;
