@@ -245,7 +245,7 @@ struct SmemStore {
 #define ADSB_FALLBACK_FILTER 1
 #endif
 #ifndef ADSB_LP_MIN_ROUNDS
-#define ADSB_LP_MIN_ROUNDS 2  // level_pick only for steps of more than this many kBT-wide rounds
+#define ADSB_LP_MIN_ROUNDS 8  // level_pick only for steps of more than this many kBT-wide rounds
 #endif
 #ifndef ADSB_LEVEL_PICK
 #define ADSB_LEVEL_PICK 1
