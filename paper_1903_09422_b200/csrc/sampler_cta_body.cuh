@@ -26,6 +26,7 @@ struct Shared {
     unsigned long long tick[2];       // next work item, double-buffered by loop parity
     uint32_t tflag[2];                // fused: the previous sample completed its epoch
     unsigned long long done_old;      // thread 0 (fused): Done counter before the last sample's increment
+    unsigned long long spare_tick;    // thread 0 (fused, ADSB_TICKET_PAIR): second ticket of the last fetch
     unsigned long long st_edges, st_rebuild, st_back, st_verts, st_degen;  // block statistics (thread 0 adds)
     unsigned long long n_samples, n_fallbacks, n_errors;
     uint32_t g_region, g_tag;         // fallback: borrowed global region and its tag
@@ -243,6 +244,9 @@ struct SmemStore {
 #endif
 #ifndef ADSB_FALLBACK_FILTER
 #define ADSB_FALLBACK_FILTER 1
+#endif
+#ifndef ADSB_TICKET_PAIR
+#define ADSB_TICKET_PAIR 0
 #endif
 #ifndef ADSB_LP_MIN_ROUNDS
 #define ADSB_LP_MIN_ROUNDS 8  // level_pick only for steps of more than this many kBT-wide rounds
@@ -1651,6 +1655,7 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
         sh.last_d = 0;
         sh.pending = 0;
         sh.done_old = 0;
+        sh.spare_tick = ~0ull;
     }
     if (kMode != kModeFused) {
         for (uint32_t it = 0;; ++it) {
@@ -1683,7 +1688,20 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
                 if (!completed) {
                     // the ticket and both control words are fetched together
                     // (three round trips in flight, not one after another)
+#if ADSB_TICKET_PAIR
+                    // two consecutive tickets per fetch: every other sample
+                    // skips the global atomic (a held spare above the stop is
+                    // dropped; its epoch is never folded)
+                    if (sh.spare_tick != ~0ull) {
+                        i = sh.spare_tick;
+                        sh.spare_tick = ~0ull;
+                    } else {
+                        i = atomicAdd(p.ctl + kCtlTicket, 2ull);
+                        sh.spare_tick = i + 1;
+                    }
+#else
                     i = atomicAdd(p.ctl + kCtlTicket, 1ull);
+#endif
                     unsigned long long stop_v = vload(p.ctl + kCtlStop), fold_v = vload(p.ctl + kCtlFolded);
                     const unsigned long long e = i / p.epoch_b;
                     for (;;) {
