@@ -16,7 +16,9 @@ checked through size-independent properties:
   frames equal the oracle's;
 * a deep, low-degree lattice with holes (C4's shape, smaller): sampled paths
   equal the oracle's on the global-state store with thread-per-vertex
-  expansion (C4 itself: test_gpu_parity.py::test_degenerate_sigma_frames_c4);
+  expansion; C4 itself: a capped full-size run equals the oracle's counts,
+  and test_gpu_parity.py::test_degenerate_sigma_frames_c4 pins the
+  all-sigma-wrapped backtrack step;
 * C5 at full size: paths identical with and without the shared-memory table,
   and the fused epoch run reproducible run to run.
 """
@@ -168,3 +170,18 @@ def test_c5_fullsize_store_invariance_and_reproducibility(c5_csr, monkeypatch):
     r2 = estimate_bc(g1, w.epsilon, w.delta, cfg)
     assert r1.tau == r2.tau == 48 * 1024 and r1.reason.name == "capped"
     np.testing.assert_array_equal(r1.run.data, r2.run.data)
+
+
+def test_c4_fullsize_capped_run_matches_oracle():
+    """C4 at full size (2048^2 lattice with holes, 4.19M vertices, sigma wraps
+    mod 2^64): a capped deterministic run on the global store (cleared layout,
+    512-thread teams, batched claims, push rebuild) gives the oracle's tau and
+    every per-vertex count."""
+    pairs = datasets.pairs("c4_grid")
+    pg, og = both(pairs)
+    cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=1, threads=8, base_seed=42, max_cycles=24, device=0)
+    r = estimate_bc(pg.graph, 0.01, 0.1, cfg)
+    o = oracle.estimate_bc(og, 0.01, 0.1, spf=1, seed=42, nominal_threads=8, max_frames=24)
+    assert (r.tau, r.run.check_cycles, r.reason.name) == (o.tau, o.check_cycles, o.reason) == (24, 24, "capped")
+    np.testing.assert_array_equal(r.run.data, o.counts)
+    assert int(r.run.data.sum()) > 24 * 500  # deep paths: hundreds of interior vertices each
