@@ -202,6 +202,7 @@ struct SmemStore {
     __device__ void set_dag(uint32_t slot) { atomicOr(&km[slot], 0x40u); }
     __device__ void prefetch(uint32_t) const {}
     static constexpr bool kBatchClaims = false;
+    static constexpr bool kSlotIsVertex = false;
     __device__ unsigned long long claim_issue(uint32_t, uint32_t) { return ~0ull; }
     template <bool kReserve = true>
     __device__ uint32_t claim_tok(uint32_t v, uint32_t new_meta, unsigned long long, bool& inserted, uint32_t& meta) {
@@ -245,6 +246,9 @@ struct SmemStore {
 #ifndef ADSB_FALLBACK_FILTER
 #define ADSB_FALLBACK_FILTER 1
 #endif
+#ifndef ADSB_SPEC_SIGMA
+#define ADSB_SPEC_SIGMA 0  // measured neutral (C4 -0.1%)
+#endif
 #ifndef ADSB_TICKET_PAIR
 #define ADSB_TICKET_PAIR 0
 #endif
@@ -264,6 +268,7 @@ template <uint32_t kU, bool kBatch = false>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
     static constexpr bool kBatchClaims = kBatch;  // global-store-only kernels
+    static constexpr bool kSlotIsVertex = true;   // find() returns the vertex as its slot
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
     static constexpr unsigned long long kPresent = 1ull << 32;
     unsigned long long* st;  // 2 words per vertex: (tag or present << 32 | meta), sigma
@@ -1177,11 +1182,20 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
                     bool cand = false;
                     if (i < end) {
                         q = C.N(i);
+#if ADSB_SPEC_SIGMA
+                        // global store: a vertex's sigma sits next to its meta word,
+                        // so both loads go out together (one round trip per step less)
+                        const unsigned long long sv = Store::kSlotIsVertex ? S.sigma(q) : 0ull;
+#endif
                         const uint32_t sl = S.find(q, m);
                         cand = sl != kNone && m_is_t(m) == want_t && m_dist(m) == want_dist &&
                                (!want_t || (m & kMetaDag));
                         if (cand) {
+#if ADSB_SPEC_SIGMA
+                            val = Store::kSlotIsVertex ? sv : S.sigma(sl);
+#else
                             val = S.sigma(sl);
+#endif
 #if ADSB_BT_PREFETCH
                             // one of the candidates is the next step's cur: its offsets
                             // line is in L1 when that step starts
