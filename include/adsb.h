@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define ADSB_ABI_VERSION 1
+#define ADSB_ABI_VERSION 2
 
 typedef enum {
     ADSB_OK = 0,
@@ -43,8 +43,18 @@ typedef enum {
 
 /* engine.hpp:63 enum class Variant. On the GPU, `indexed` (and `sequential`,
  * which run_sequential keys as one stream, engine.hpp:238 — not bit-comparable)
- * run the deterministic frame pipeline; `barrier`, `local` and `shared` run the
- * cumulative epoch pipeline (ADSB_MODE_NONDET). */
+ * run the deterministic frame pipeline. `barrier`, `local` and `shared` run
+ * cumulative epochs (the stop rule on the running total after every epoch):
+ *   shared, local  epochs of epoch_samples (default 1024) samples; sample i
+ *                  drawn from stream_rng(seed, i). One GPU: one persistent
+ *                  kernel folds epochs in order. Several GPUs: sample indices
+ *                  are sharded, each rank's per-sample increments are
+ *                  all-gathered and every rank folds them in index order, so
+ *                  tau and the counts equal the one-GPU run's at any GPU count;
+ *   barrier        rounds of check_interval samples (run_barrier's N,
+ *                  engine.hpp:267-341) unless epoch_samples is set; several
+ *                  GPUs split each round and all-reduce the n-length count
+ *                  vector (NCCL) before every check. */
 typedef enum {
     ADSB_VARIANT_SEQUENTIAL = 0,
     ADSB_VARIANT_BARRIER = 1,
@@ -56,7 +66,21 @@ typedef enum {
 typedef enum { ADSB_REASON_EPS_CONVERGED = 0, ADSB_REASON_OMEGA_REACHED = 1, ADSB_REASON_CAPPED = 2 } adsb_reason;
 
 typedef struct adsb_graph adsb_graph; /* graph.hpp:29-76 Graph (+ ParsedGraph::original_ids) */
-typedef struct adsb_comm adsb_comm;   /* NCCL communicator, one rank per GPU */
+typedef struct adsb_comm adsb_comm;   /* one rank per GPU: NCCL or host-callback transport */
+
+typedef enum { ADSB_REDUCE_SUM = 0, ADSB_REDUCE_MAX = 1, ADSB_REDUCE_MIN = 2 } adsb_reduce_op;
+
+/* Host transport for adsb_comm_init_host: collectives over HOST memory supplied
+ * by the caller (e.g. torch.distributed with gloo), called from the thread
+ * that called adsb_estimate_bc, in the same order on every rank. Each returns
+ * 0 on success. */
+typedef struct {
+    /* in place: buf[i] = op over ranks of buf[i] */
+    int (*allreduce_u64)(void *user, uint64_t *buf, size_t count, int op /* adsb_reduce_op */);
+    int (*allreduce_u32_sum)(void *user, uint32_t *buf, size_t count);
+    /* recv[r * count + i] = rank r's send[i] */
+    int (*allgather_u64)(void *user, const uint64_t *send, uint64_t *recv, size_t count);
+} adsb_host_collectives;
 
 /* engine.hpp:85-96 EngineConfig, plus the GPU pipeline knobs. */
 typedef struct {
@@ -73,6 +97,14 @@ typedef struct {
     int32_t device;              /* CUDA ordinal; -1 = current device */
     uint32_t flags;              /* reserved, must be 0 */
     adsb_comm *comm;             /* NULL = single GPU */
+    /* engine.hpp:92-94 (indexed). bounded_memory != 0 caps the frames sampled
+     * ahead of the ordered cutoff at (reservation_block + 1) per sampler team
+     * (run_indexed's reserve_indices block, engine.hpp:137-144): less event
+     * memory, more batches; results are identical. queue_high_water sets
+     * adsb_stats.queue_high_water_exceeded. */
+    uint32_t bounded_memory;
+    uint32_t reservation_block;  /* a >= 1 */
+    uint64_t queue_high_water;
 } adsb_config;
 
 /* kadabra.hpp:295-304 BcResult + engine.hpp:163-171 RunResult scalars. */
@@ -96,6 +128,13 @@ typedef struct {
     uint64_t store_fallbacks;    /* samples redone with global-memory state (shared-memory table overflow) */
     uint64_t degenerate_steps;   /* backtrack steps whose sigma and every predecessor sigma were 0 mod 2^64
                                     (undefined in the reference) */
+    /* engine.hpp:156-161 QueueStats, per sampler team: frames sampled ahead of
+     * the in-order consumption point (deterministic batches / epoch ring) */
+    uint64_t queue_max_depth;
+    double queue_mean_depth;
+    uint64_t queue_allocated;    /* frame slots the pipeline allocated */
+    uint32_t queue_high_water_exceeded;
+    uint32_t world;              /* ranks that took part */
 } adsb_stats;
 
 void adsb_config_init(adsb_config *cfg); /* reference defaults (engine.hpp:85-96) */
@@ -160,6 +199,10 @@ adsb_status adsb_exact_bc(const adsb_graph *g, int device, double *bc /* n */, d
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------------- */
 adsb_status adsb_comm_unique_id(uint8_t id[128]);
 adsb_status adsb_comm_init(int nranks, int rank, const uint8_t id[128], int device, adsb_comm **out);
+/* the same ranks over caller-supplied host collectives (see adsb_host_collectives);
+ * ops is copied, user is passed back to every call */
+adsb_status adsb_comm_init_host(int nranks, int rank, int device, const adsb_host_collectives *ops, void *user,
+                                adsb_comm **out);
 void adsb_comm_destroy(adsb_comm *comm);
 
 /* ---- synthetic inputs (BASELINE.json configs) ---------------- */

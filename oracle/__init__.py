@@ -84,6 +84,8 @@ def lib() -> C.CDLL:
         L.or_sample_frame.restype = C.c_uint64
         L.or_estimate_bc.argtypes = [gp, C.c_double, C.c_double, C.POINTER(_Config), u64p,
                                      C.POINTER(C.c_double), C.POINTER(_Result), C.c_char_p, C.c_size_t]
+        L.or_estimate_bc_threads.argtypes = [gp, C.c_double, C.c_double, C.POINTER(_Config), C.c_int, u64p,
+                                             C.POINTER(C.c_double), C.POINTER(_Result), C.c_char_p, C.c_size_t]
         L.or_brandes.argtypes = [gp, C.POINTER(C.c_double), C.c_int]
         L.or_brandes.restype = None
         _lib = L
@@ -203,8 +205,26 @@ def kadabra_check(data, num: int, omega: int, eps: float, delta_v: float) -> boo
     return bool(out.value)
 
 
-def sample_frames(g: Graph, seed: int, spf: int, first: int, count: int) -> list[np.ndarray]:
+def sample_frames(g: Graph, seed: int, spf: int, first: int, count: int, threads: int = 1) -> list[np.ndarray]:
     lab, _ = components(g)
+    if threads > 1:
+        lens = np.zeros(max(count, 1), np.uint64)
+        u32, u64 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+        fn = lib().or_sample_frames_threads
+        fn.argtypes = [C.POINTER(_Graph), u32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, u64, u32,
+                       C.c_uint64]
+        fn.restype = C.c_uint64
+        cap = max(1024, count * 64)
+        ids = np.empty(cap, np.uint32)
+        total = fn(C.byref(g._g), lab.ctypes.data_as(u32), seed, spf, first, count, threads, lens.ctypes.data_as(u64),
+                   ids.ctypes.data_as(u32), cap)
+        if total > cap:  # rerun with room for every increment
+            cap = int(total)
+            ids = np.empty(cap, np.uint32)
+            fn(C.byref(g._g), lab.ctypes.data_as(u32), seed, spf, first, count, threads, lens.ctypes.data_as(u64),
+               ids.ctypes.data_as(u32), cap)
+        bounds = np.concatenate([[0], np.cumsum(lens[:count])]).astype(np.int64)
+        return [ids[bounds[i]:bounds[i + 1]].copy() for i in range(count)]
     sc = lib().or_scratch_new(g.n)
     out = []
     cap = max(1024, g.n * 4)
@@ -240,13 +260,20 @@ class Result:
 
 
 def estimate_bc(g: Graph, eps: float, delta: float, *, mode: int = MODE_INDEXED, spf: int = 1,
-                epoch_samples: int = 1, seed: int = 1, nominal_threads: int = 1, max_frames: int = 0) -> Result:
+                epoch_samples: int = 1, seed: int = 1, nominal_threads: int = 1, max_frames: int = 0,
+                threads: int = 1) -> Result:
+    """threads > 1: frames sampled in parallel and folded in position order
+    (or_estimate_bc_threads); results identical to threads = 1."""
     cfg = _Config(mode, nominal_threads, spf, epoch_samples, seed, max_frames, 0.5)
     counts = np.empty(max(g.n, 1), np.uint64)
     scores = np.empty(max(g.n, 1), np.float64)
     res = _Result()
     err = C.create_string_buffer(256)
-    rc = lib().or_estimate_bc(C.byref(g._g), eps, delta, C.byref(cfg), counts.ctypes.data_as(C.POINTER(C.c_uint64)),
+    fn = lib().or_estimate_bc
+    extra = ()
+    if threads > 1:
+        fn, extra = lib().or_estimate_bc_threads, (threads,)
+    rc = fn(C.byref(g._g), eps, delta, C.byref(cfg), *extra, counts.ctypes.data_as(C.POINTER(C.c_uint64)),
                               scores.ctypes.data_as(C.POINTER(C.c_double)), C.byref(res), err, 256)
     if rc:
         raise OracleError(rc, err.value.decode())
@@ -258,6 +285,37 @@ def brandes(g: Graph, threads: int | None = None) -> np.ndarray:
     bc = np.empty(max(g.n, 1), np.float64)
     lib().or_brandes(C.byref(g._g), bc.ctypes.data_as(C.POINTER(C.c_double)), threads or os.cpu_count() or 1)
     return bc[: g.n]
+
+
+GEN_KINDS = {"gnm": 0, "rmat": 1, "ba": 2, "grid": 3}
+
+
+def gen_pairs(kind: str, params, lcc: bool = True) -> np.ndarray:
+    """The benchmark graphs from gen.c (independent of libadsb.so; equal to
+    paper_1903_09422_b200.datasets' generators, tests/test_oracle.py)."""
+    L = lib()
+    fn = L.or_gen_pairs
+    fn.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_uint64)]
+    fn.restype = C.POINTER(C.c_uint64)
+    L.or_free.argtypes = [C.c_void_p]
+    L.or_free.restype = None
+    par = (C.c_double * 8)(*[float(x) for x in params])
+    m = C.c_uint64()
+    ptr = fn(GEN_KINDS[kind], par, int(lcc), C.byref(m))
+    if not ptr:
+        return np.zeros(0, np.uint64)
+    out = np.ctypeslib.as_array(ptr, shape=(2 * m.value,)).copy() if m.value else np.zeros(0, np.uint64)
+    L.or_free(C.cast(ptr, C.c_void_p))
+    return out
+
+
+def write_dense_edges(path, pairs: np.ndarray) -> None:
+    """u32 n, u64 m, m x (u32, u32) first-appearance dense ids (ref_driver --graph-bin)."""
+    a = np.ascontiguousarray(pairs, dtype=np.uint64)
+    fn = lib().or_write_dense_edges
+    fn.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.c_uint64]
+    if fn(os.fsencode(str(path)), a.ctypes.data_as(C.POINTER(C.c_uint64)), a.shape[0] // 2):
+        raise OracleError(1, f"cannot write {path}")
 
 
 def fnv1a(counts: np.ndarray) -> str:
@@ -276,14 +334,19 @@ def ref_available() -> bool:
 
 def ref_run(graph_path, *, eps: float, delta: float, seed: int, variant: str = "indexed", spf: int = 1,
             threads: int = 1, check_interval: int = 1000, max_cycles: int = 0, counts_path=None,
-            timeout: float | None = None, reps: int = 1) -> dict:
-    cmd = [str(REF_DRIVER), "run", "--graph", str(graph_path), "--eps", repr(eps), "--delta", repr(delta),
+            timeout: float | None = None, reps: int = 1, graph_flag: str = "--graph") -> dict:
+    cmd = [str(REF_DRIVER), "run", graph_flag, str(graph_path), "--eps", repr(eps), "--delta", repr(delta),
            "--seed", str(seed), "--variant", variant, "--spf", str(spf), "--threads", str(threads),
            "--check-interval", str(check_interval), "--max-cycles", str(max_cycles), "--reps", str(reps)]
     if counts_path:
         cmd += ["--counts", str(counts_path)]
     out = subprocess.run(cmd, capture_output=True, text=True, check=True, timeout=timeout)
     return json.loads(out.stdout)
+
+
+def ref_run_bin(graph_path, **kw) -> dict:
+    """ref_run on a dense-pairs file (write_dense_edges), ingested by Graph::from_edges."""
+    return ref_run(graph_path, graph_flag="--graph-bin", **kw)
 
 
 def ref_frames(graph_path, *, seed: int, spf: int, first: int, count: int, out_path) -> list[np.ndarray]:

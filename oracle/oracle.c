@@ -787,3 +787,218 @@ void or_brandes(const or_graph *g, double *bc, int threads) {
     free(jobs);
     free(tids);
 }
+
+/* ------------------------------------------------------------------------ */
+/* or_estimate_bc_threads: or_estimate_bc's semantics (run_indexed,          */
+/* engine.hpp:490-643, or the cumulative epochs) computed by T threads the   */
+/* way run_indexed itself parallelises: frames are sampled independently     */
+/* (each from its own stream_rng(seed, p), engine.hpp:595-610) and folded    */
+/* strictly in position order by one thread, which evaluates kadabra_check   */
+/* after every cycle (engine.hpp:544-565). Results are identical to          */
+/* or_estimate_bc at any T. The check first evaluates f/g at the largest     */
+/* count: if that vertex fails, kadabra_converged (kadabra.hpp:133-144) is   */
+/* false exactly (it scans that vertex too); otherwise the full scan runs.   */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const or_graph *g;
+    const uint32_t *label;
+    uint64_t seed, spf, first, count;
+    uint32_t **buf;      /* per frame: increments (malloc'ed) */
+    uint64_t *len;       /* per frame */
+    uint64_t next;       /* work counter (atomic) */
+    scratch_t *sc;       /* per worker */
+    uint32_t *tmp;       /* per worker, n + 1 */
+} frames_job;
+
+typedef struct {
+    frames_job *job;
+    int id;
+} frames_worker_arg;
+
+static void *frames_worker(void *argp) {
+    frames_worker_arg *a = argp;
+    frames_job *j = a->job;
+    scratch_t *sc = &j->sc[a->id];
+    uint32_t *tmp = j->tmp + (size_t)a->id * ((size_t)j->g->n + 1);
+    for (;;) {
+        const uint64_t i = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+        if (i >= j->count) break;
+        uint64_t rng = or_reseed(j->seed, j->first + i);
+        uint64_t cap = 64, len = 0;
+        uint32_t *out = malloc(cap * sizeof(uint32_t));
+        for (uint64_t k = 0; k < j->spf; ++k) {
+            const uint32_t m = or_sample_path(j->g, j->label, &rng, tmp, sc);
+            if (len + m > cap) {
+                while (len + m > cap) cap *= 2;
+                out = realloc(out, cap * sizeof(uint32_t));
+            }
+            memcpy(out + len, tmp, (size_t)m * sizeof(uint32_t));
+            len += m;
+        }
+        j->buf[i] = out;
+        j->len[i] = len;
+    }
+    return NULL;
+}
+
+int or_estimate_bc_threads(const or_graph *g, double eps, double delta, const or_config *cfg, int threads,
+                           uint64_t *counts, double *scores, or_result *res, char *err, size_t errlen) {
+    if (threads <= 1 || g->n <= 1) return or_estimate_bc(g, eps, delta, cfg, counts, scores, res, err, errlen);
+    memset(res, 0, sizeof(*res));
+    const uint32_t n = g->n;
+    if (cfg->samples_per_frame < 1 || cfg->nominal_threads < 1) {
+        SET_ERR("samples per frame must be >= 1");
+        return OR_EINVAL;
+    }
+    if (cfg->mode == OR_MODE_EPOCH && cfg->epoch_samples < 1) {
+        SET_ERR("epoch samples must be >= 1");
+        return OR_EINVAL;
+    }
+    uint32_t *label = malloc((size_t)n * sizeof(uint32_t));
+    or_connected_components(g, label);
+    const uint64_t dub = or_diameter_upper_bound(g);
+    uint64_t omega = 0;
+    if (or_compute_omega(dub, eps, delta, cfg->c, &omega)) {
+        SET_ERR("epsilon and delta must lie in (0,1)");
+        free(label);
+        return OR_EINVAL;
+    }
+    const double delta_v = delta / (2.0 * (double)n); /* kadabra.hpp:34 */
+    const double log_inv = log(1.0 / delta_v);        /* kadabra.hpp:123 */
+    const int epoch_mode = cfg->mode == OR_MODE_EPOCH;
+    const uint64_t per_cycle = epoch_mode ? cfg->epoch_samples : 1; /* frames per check */
+    const uint64_t spf = epoch_mode ? 1 : cfg->samples_per_frame;
+
+    uint64_t *data = calloc(n, sizeof(uint64_t));
+    scratch_t *sc = calloc((size_t)threads, sizeof(scratch_t));
+    for (int t = 0; t < threads; ++t) {
+        scratch_t *s = or_scratch_new(n);
+        sc[t] = *s;
+        free(s);
+    }
+    uint32_t *tmp = malloc((size_t)threads * ((size_t)n + 1) * sizeof(uint32_t));
+    /* ~64 samples per worker per batch; frames past the stop are discarded */
+    const uint64_t batch = (uint64_t)threads * (spf >= 64 ? 1 : 64 / spf);
+    uint32_t **buf = calloc(batch, sizeof(uint32_t *));
+    uint64_t *lens = calloc(batch, sizeof(uint64_t));
+    pthread_t *tids = calloc((size_t)threads, sizeof(pthread_t));
+    frames_worker_arg *args = calloc((size_t)threads, sizeof(frames_worker_arg));
+
+    uint64_t num = 0, cycles = 0, stop_epoch = 0, position = 0, max_count = 0, in_cycle = 0;
+    int reason_capped = 0, done = 0;
+    while (!done) {
+        frames_job job = {g, label, cfg->seed, spf, position, batch, buf, lens, 0, sc, tmp};
+        for (int t = 0; t < threads; ++t) {
+            args[t].job = &job;
+            args[t].id = t;
+            pthread_create(&tids[t], NULL, frames_worker, &args[t]);
+        }
+        for (int t = 0; t < threads; ++t) pthread_join(tids[t], NULL);
+        for (uint64_t i = 0; i < batch; ++i) {
+            if (!done) {
+                for (uint64_t k = 0; k < lens[i]; ++k) {
+                    const uint64_t c = ++data[buf[i][k]];
+                    if (c > max_count) max_count = c;
+                }
+                num += spf;
+                if (++in_cycle == per_cycle) {
+                    in_cycle = 0;
+                    ++cycles;
+                    /* kadabra.hpp:148-151 */
+                    int stop = num >= omega;
+                    if (!stop) {
+                        const double b = (double)max_count / (double)num;
+                        if (f_kernel(b, log_inv, (double)omega, (double)num) <= eps &&
+                            g_kernel(b, log_inv, (double)omega, (double)num) <= eps)
+                            stop = converged(data, n, num, omega, eps, log_inv);
+                    }
+                    if (stop || (cfg->max_frames && cycles >= cfg->max_frames)) {
+                        reason_capped = !stop;
+                        stop_epoch = epoch_mode ? cycles : (cycles - 1) / cfg->nominal_threads + 1;
+                        done = 1;
+                    }
+                }
+            }
+            free(buf[i]);
+            buf[i] = NULL;
+        }
+        position += batch;
+    }
+    res->tau = num;
+    res->check_cycles = cycles;
+    res->stop_epoch = stop_epoch;
+    res->omega = omega;
+    res->diameter_bound = dub;
+    res->total_samples = num;
+    for (int t = 0; t < threads; ++t) {
+        res->edges_scanned += sc[t].edges_scanned;
+        res->vertices_expanded += sc[t].vertices_expanded;
+        res->degenerate_steps += sc[t].degenerate_steps;
+    }
+    res->reason = OR_REASON_OMEGA;
+    if (num >= 1 && converged(data, n, num, omega, eps, log_inv)) res->reason = OR_REASON_EPS;
+    if (reason_capped) res->reason = OR_REASON_CAPPED;
+    for (uint32_t v = 0; v < n; ++v) {
+        if (counts) counts[v] = data[v];
+        if (scores) scores[v] = num == 0 ? 0.0 : (double)data[v] / (double)num;
+    }
+    for (int t = 0; t < threads; ++t) {
+        free(sc[t].stamp);
+        free(sc[t].dist);
+        free(sc[t].sigma);
+        free(sc[t].queue);
+    }
+    free(sc);
+    free(tmp);
+    free(buf);
+    free(lens);
+    free(tids);
+    free(args);
+    free(data);
+    free(label);
+    return OR_OK;
+}
+
+/* Frames [first, first+count) by `threads` workers (or_sample_frame per frame,
+ * engine.hpp:595-610 keying). lens[i] = increments of frame i; ids receives the
+ * concatenation (up to cap). Returns the total number of increments. */
+uint64_t or_sample_frames_threads(const or_graph *g, const uint32_t *label, uint64_t seed, uint64_t spf,
+                                  uint64_t first, uint64_t count, int threads, uint64_t *lens, uint32_t *ids,
+                                  uint64_t cap) {
+    if (threads < 1) threads = 1;
+    scratch_t *sc = calloc((size_t)threads, sizeof(scratch_t));
+    for (int t = 0; t < threads; ++t) {
+        scratch_t *s = or_scratch_new(g->n);
+        sc[t] = *s;
+        free(s);
+    }
+    uint32_t *tmp = malloc((size_t)threads * ((size_t)g->n + 1) * sizeof(uint32_t));
+    uint32_t **buf = calloc(count ? count : 1, sizeof(uint32_t *));
+    frames_job job = {g, label, seed, spf, first, count, buf, lens, 0, sc, tmp};
+    pthread_t *tids = calloc((size_t)threads, sizeof(pthread_t));
+    frames_worker_arg *args = calloc((size_t)threads, sizeof(frames_worker_arg));
+    for (int t = 0; t < threads; ++t) {
+        args[t].job = &job;
+        args[t].id = t;
+        pthread_create(&tids[t], NULL, frames_worker, &args[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tids[t], NULL);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        for (uint64_t k = 0; k < lens[i]; ++k, ++total)
+            if (total < cap) ids[total] = buf[i][k];
+        free(buf[i]);
+    }
+    for (int t = 0; t < threads; ++t) {
+        free(sc[t].stamp);
+        free(sc[t].dist);
+        free(sc[t].sigma);
+        free(sc[t].queue);
+    }
+    free(sc);
+    free(tmp);
+    free(buf);
+    free(tids);
+    free(args);
+    return total;
+}

@@ -60,6 +60,9 @@ class Config(C.Structure):
         ("device", C.c_int32),
         ("flags", C.c_uint32),
         ("comm", C.c_void_p),
+        ("bounded_memory", C.c_uint32),
+        ("reservation_block", C.c_uint32),
+        ("queue_high_water", C.c_uint64),
     ]
 
 
@@ -83,7 +86,23 @@ class Stats(C.Structure):
         ("backtrack_edges", C.c_uint64),
         ("store_fallbacks", C.c_uint64),
         ("degenerate_steps", C.c_uint64),
+        ("queue_max_depth", C.c_uint64),
+        ("queue_mean_depth", C.c_double),
+        ("queue_allocated", C.c_uint64),
+        ("queue_high_water_exceeded", C.c_uint32),
+        ("world", C.c_uint32),
     ]
+
+
+# include/adsb.h adsb_host_collectives
+HOST_ALLREDUCE_U64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t, C.c_int)
+HOST_ALLREDUCE_U32_SUM = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint32), C.c_size_t)
+HOST_ALLGATHER_U64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_size_t)
+
+
+class HostCollectives(C.Structure):
+    _fields_ = [("allreduce_u64", HOST_ALLREDUCE_U64), ("allreduce_u32_sum", HOST_ALLREDUCE_U32_SUM),
+                ("allgather_u64", HOST_ALLGATHER_U64)]
 
 
 P = C.c_void_p
@@ -120,6 +139,7 @@ _SIGS = {
     "adsb_sample_frames": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u32p, C.c_uint64]),
     "adsb_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "adsb_comm_init": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(P)]),
+    "adsb_comm_init_host": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(HostCollectives), P, C.POINTER(P)]),
     "adsb_comm_destroy": (None, [P]),
     "adsb_gen_gnm": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(u64p), u64p]),
     "adsb_gen_rmat": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int,

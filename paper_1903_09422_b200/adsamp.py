@@ -137,6 +137,9 @@ class EngineConfig:
         c.max_cycles = self.max_cycles
         c.device = self.device
         c.comm = getattr(self.comm, "handle", None)
+        c.bounded_memory = int(bool(self.bounded_memory))
+        c.reservation_block = self.reservation_block
+        c.queue_high_water = self.queue_high_water
         return c
 
 
@@ -174,6 +177,16 @@ def reserve_indices(counter: ReservationCounter, T: int, a: int) -> list[int]:
 
 
 @dataclass
+class QueueStats:
+    """engine.hpp:156-161, per sampler team: frames sampled ahead of the in-order
+    consumption point (deterministic batches, epoch ring)."""
+    max_depth: int = 0
+    mean_depth: float = 0.0
+    allocated: int = 0
+    high_water_exceeded: bool = False
+
+
+@dataclass
 class RunResult:
     """engine.hpp:163-171"""
     data: np.ndarray
@@ -182,6 +195,7 @@ class RunResult:
     per_thread_samples: list = field(default_factory=list)
     check_cycles: int = 0
     stop_epoch: int = 0
+    queue: QueueStats = field(default_factory=QueueStats)
 
 
 # --------------------------------------------------------------------------- graph.hpp

@@ -66,6 +66,7 @@ void validate(const adsb_config& c) {
     if (c.check_interval < 1) invalid("check interval must be >= 1");
     if (!(c.latency_exponent > 0)) invalid("xi must be > 0");
     if (c.samples_per_frame < 1) invalid("samples per frame must be >= 1");
+    if (c.reservation_block < 1) invalid("reservation block must be >= 1");
     if (c.variant < ADSB_VARIANT_SEQUENTIAL || c.variant > ADSB_VARIANT_INDEXED) invalid("unknown variant");
     if (c.flags != 0) invalid("flags must be 0");
 }
@@ -97,6 +98,9 @@ void adsb_config_init(adsb_config* cfg) {
     cfg->max_cycles = 0;
     cfg->device = -1;
     cfg->comm = nullptr;
+    cfg->bounded_memory = 0;
+    cfg->reservation_block = 4;
+    cfg->queue_high_water = 64;
 }
 
 adsb_status adsb_graph_parse_text(const char* text, uint64_t len, adsb_graph** out) {
@@ -315,8 +319,13 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
         if (g->host.n == 0) invalid("graph has no vertices");  // kadabra.hpp:310
         EngineOptions opt;
         opt.deterministic = cfg->variant == ADSB_VARIANT_INDEXED || cfg->variant == ADSB_VARIANT_SEQUENTIAL;
+        opt.barrier = cfg->variant == ADSB_VARIANT_BARRIER;
         opt.spf = cfg->samples_per_frame;
         opt.epoch_samples = cfg->epoch_samples;
+        opt.check_interval = cfg->check_interval;
+        opt.bounded_memory = cfg->bounded_memory != 0;
+        opt.reservation_block = cfg->reservation_block;
+        opt.queue_high_water = cfg->queue_high_water;
         opt.seed = cfg->base_seed;
         opt.max_cycles = cfg->max_cycles;
         opt.nominal_threads = cfg->variant == ADSB_VARIANT_SEQUENTIAL ? 1 : cfg->threads;
@@ -357,6 +366,11 @@ adsb_status adsb_estimate_bc(const adsb_graph* g, double epsilon, double delta, 
             stats->backtrack_edges = r.backtrack_edges;
             stats->store_fallbacks = r.store_fallbacks;
             stats->degenerate_steps = r.degenerate_steps;
+            stats->queue_max_depth = r.queue_max_depth;
+            stats->queue_mean_depth = r.queue_mean_depth;
+            stats->queue_allocated = r.queue_allocated;
+            stats->queue_high_water_exceeded = r.queue_high_water_exceeded ? 1u : 0u;
+            stats->world = r.world;
         }
     });
 }
@@ -412,11 +426,25 @@ adsb_status adsb_comm_init(int nranks, int rank, const uint8_t id[128], int devi
     });
 }
 
-void adsb_comm_destroy(adsb_comm* comm) {
-    if (!comm) return;
-    if (comm->comm) ncclCommDestroy(comm->comm);
-    delete comm;
+adsb_status adsb_comm_init_host(int nranks, int rank, int device, const adsb_host_collectives* ops, void* user,
+                                adsb_comm** out) {
+    return guard([&] {
+        need(ops, "ops");
+        need(out, "out");
+        if (!ops->allreduce_u64 || !ops->allreduce_u32_sum || !ops->allgather_u64)
+            invalid("every host collective must be set");
+        if (nranks < 1 || rank < 0 || rank >= nranks) invalid("rank out of range");
+        auto c = std::make_unique<adsb_comm>();
+        c->host = *ops;
+        c->user = user;
+        c->nranks = nranks;
+        c->rank = rank;
+        c->device = resolve_device(device);
+        *out = c.release();
+    });
 }
+
+void adsb_comm_destroy(adsb_comm* comm) { delete comm; }
 
 static adsb_status hand_out(std::vector<uint64_t>&& v, uint64_t** pairs, uint64_t* count) {
     need(pairs, "pairs");

@@ -99,11 +99,13 @@ __global__ void k_event_values(const unsigned long long* __restrict__ sorted, ui
 }
 
 // K4b: first frame of the batch at which the rule holds (or the cap frame)
+// (frames_before is a multiple of C; the rule is evaluated after every C-th frame)
 __global__ void k_find_stop(const uint32_t* __restrict__ run_max, uint32_t frames,
-                            const uint32_t* base_max, uint64_t frames_before, uint64_t spf,
+                            const uint32_t* base_max, uint64_t frames_before, uint64_t spf, uint64_t C,
                             RuleParams r, uint32_t* stop) {
     const uint32_t bm = *base_max;
     for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < frames; f += gridDim.x * blockDim.x) {
+        if ((f + 1) % C != 0) continue;
         const uint64_t tau = (frames_before + f + 1) * spf;
         if (rule_passes(max(run_max[f], bm), tau, r)) atomicMin(stop, f);
     }
@@ -387,6 +389,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     }
     const int world = opt.comm ? opt.comm->nranks : 1;
     const int rank = opt.comm ? opt.comm->rank : 0;
+    out.world = static_cast<uint32_t>(world);
 
     // ---- preprocessing (kadabra.hpp:319-325): components, D_ub, omega, deltas
     Timer pre;
@@ -398,6 +401,11 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     out.diameter_bound = device_diameter_bound(ctx);
     const double t_dub = pre.seconds();
     out.omega = compute_omega(out.diameter_bound, eps, delta, opt.c);
+    // Device counts are u32 (every count is <= tau <= omega): refuse runs whose
+    // omega does not fit rather than wrap (the reference's data[] is u64,
+    // frame.hpp:118; omega >= 2^32 needs eps below ~5e-5)
+    if (out.omega > 0xFFFFFFFFull)
+        invalid("omega = " + std::to_string(out.omega) + " exceeds 2^32-1 (u32 device counts); raise epsilon");
     const double delta_v = delta / (2.0 * static_cast<double>(n));  // kadabra.hpp:34
     const double log_inv = std::log(1.0 / delta_v);                 // kadabra.hpp:123
     const uint32_t level_cap = static_cast<uint32_t>(std::min<uint64_t>(out.diameter_bound + 3, n + 2));
@@ -430,176 +438,54 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     const uint32_t* max_dev32 = nullptr;  // device copy of max_v counts[v] when a branch keeps one
     bool max_known = false;
     uint64_t max_host = 0;
-    // work units that keep every team busy: warps are many and light, blocks few and heavy
-    const uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).blocks;
+    // work units that keep every team busy: warps are many and light, blocks few
+    // and heavy. Batch and epoch sizes derive from it, and every rank must make
+    // the same sizing decisions (they set the collectives' sizes and order), so
+    // ranks agree on the smallest.
+    uint64_t team_slots = arena(ctx).kind == 0 ? arena(ctx).slots : 8ull * arena(ctx).blocks;
+    if (world > 1) comm_allreduce_host(opt.comm, &team_slots, 1, RedOp::kMin, s1);
 
-    if (opt.deterministic && !opt.comm && std::getenv("ADSB_DET_PIPELINE")) {
-        // ---- deterministic frames, pipelined: while the host reads batch b's
-        // event count and stream 2 runs its ordered cutoff, stream 1 already
-        // samples batch b+1 (speculatively; wasted if b stops). Two event
-        // buffers alternate; a buffer is reused only after its cutoff applied.
-        const uint64_t spf = opt.spf;
+    // Pipelines. Deterministic variants: frames of spf samples, the rule after
+    // every frame (run_indexed). Non-deterministic variants: cumulative epochs of
+    // B samples (sample i from stream_rng(seed, i)), the rule after every epoch:
+    //  * one GPU, block teams: one persistent kernel folds epochs in order (fused);
+    //  * barrier on several GPUs: run_barrier's rounds, each split across the
+    //    ranks and combined by an all-reduce of the n-length count vector;
+    //  * otherwise (several GPUs, or warp teams): the frame pipeline with spf = 1
+    //    and the rule evaluated at epoch ends only — the ranks' per-sample
+    //    increments are all-gathered and folded in index order, so tau and the
+    //    counts do not depend on the GPU count.
+    // All non-det paths give identical results for the same B.
+    const uint64_t epoch_B = opt.epoch_samples ? opt.epoch_samples : (opt.barrier ? opt.check_interval : 1024);
+    const bool fused_mode = !opt.deterministic && world == 1 && arena(ctx).kind == 1 && !std::getenv("ADSB_NO_FUSED");
+    const bool dense_mode = !opt.deterministic && !fused_mode && (opt.barrier || std::getenv("ADSB_DENSE_EPOCHS")) &&
+                            (world > 1 || std::getenv("ADSB_DENSE_EPOCHS"));
+    const bool frames_mode = opt.deterministic || (!fused_mode && !dense_mode);
+    // queue statistics (engine.hpp:156-161): frames sampled ahead of the in-order
+    // consumption point, per sampler team
+    const uint64_t teams = std::max<uint64_t>(arena(ctx).kind == 0 ? team_slots : team_slots / 8, 1) * world;
+    const double teams_total = static_cast<double>(teams);
+    uint64_t depth_obs = 0;
+    double depth_sum = 0;
+    auto observe_depth = [&](uint64_t frames_ahead) {
+        const uint64_t d = static_cast<uint64_t>(std::ceil(static_cast<double>(frames_ahead) / teams_total));
+        out.queue_max_depth = std::max(out.queue_max_depth, d);
+        depth_sum += static_cast<double>(d);
+        ++depth_obs;
+        out.queue_allocated = std::max(out.queue_allocated, frames_ahead);
+    };
+
+    if (frames_mode) {
+        // C = frames per check: 1 (run_indexed), or B single-sample frames (epochs)
+        const uint64_t spf = opt.deterministic ? opt.spf : 1;
+        const uint64_t C = opt.deterministic ? 1 : epoch_B;
         uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
-        if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
-        frame_limit = std::max<uint64_t>(frame_limit, 1);
-        uint32_t* base_max = ctx.rt->pool.get<uint32_t>(Scratch::kBaseMax, 1);
-        uint32_t* stop_idx = ctx.rt->pool.get<uint32_t>(Scratch::kStopIdx, 1);
-        uint32_t* stop_h = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinStop);
-        unsigned long long* cursor_h = ctx.rt->pinned.ptr + kPinCursor;
-        ADSB_CUDA(cudaMemsetAsync(base_max, 0, sizeof(uint32_t), s1));
-        const Scratch ev_id[2] = {Scratch::kEvents, Scratch::kEvents2};
-        unsigned long long* ev_buf[2] = {ctx.rt->pool.get<unsigned long long>(ev_id[0], 1 << 20),
-                                         ctx.rt->pool.get<unsigned long long>(ev_id[1], 1 << 20)};
-        unsigned long long* scal2 = ctx.rt->pool.get<unsigned long long>(Scratch::kScal2, 4);
-        if (!ctx.rt->ev_samp[0]) {
-            for (int i = 0; i < 2; ++i) {
-                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_samp[i], cudaEventDisableTiming));
-                ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_chk[i], cudaEventDisableTiming));
-            }
-            ADSB_CUDA(cudaEventCreateWithFlags(&ctx.rt->ev_stat, cudaEventDisableTiming));
-        }
-        cudaEvent_t* ev_sampled = ctx.rt->ev_samp;
-        cudaEvent_t* ev_free = ctx.rt->ev_chk;
-        bool slot_used[2] = {false, false};
-        struct Batch {
-            uint64_t first = 0, F = 0;
-            int slot = 0;
-            uint64_t launch = 0;
-        };
-        uint64_t next_first = 0, sampled_frames = 0, launches = 0;
-        auto plan = [&](Batch& b, int slot) -> bool {
-            if (next_first >= frame_limit) return false;
-            uint64_t F = std::max<uint64_t>(2 * team_slots, next_first);
-            F = std::min<uint64_t>(F, frame_limit - next_first);
-            F = std::min<uint64_t>(F, 1ull << 30);
-            b.first = next_first;
-            b.F = F;
-            b.slot = slot;
-            next_first += F;
-            return true;
-        };
-        auto enqueue = [&](Batch& b) {
-            const int j = b.slot;
-            if (slot_used[j]) ADSB_CUDA(cudaStreamWaitEvent(s1, ev_free[j], 0));
-            slot_used[j] = true;
-            ADSB_CUDA(cudaMemsetAsync(scal2 + 2 * j, 0, 2 * sizeof(unsigned long long), s1));
-            SamplerParams p = base_params(ctx, opt.seed, spf);
-            p.first = b.first;
-            p.num_items = b.F;
-            p.ticket = scal2 + 2 * j;
-            p.ev_cursor = scal2 + 2 * j + 1;
-            p.events = ev_buf[j];
-            p.ev_cap = ctx.rt->pool.capacity<unsigned long long>(ev_id[j]);
-            p.stats = stats;
-            while (ctx.rt->ev_launch.size() < 2 * (launches + 1)) {
-                cudaEvent_t ev;
-                ADSB_CUDA(cudaEventCreate(&ev));
-                ctx.rt->ev_launch.push_back(ev);
-            }
-            b.launch = launches++;
-            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * b.launch], s1));
-            launch_sampler(static_cast<SamplerKind>(arena(ctx).kind == 0 ? 0 : 1), true, p, s1);
-            ADSB_CUDA(cudaEventRecord(ctx.rt->ev_launch[2 * b.launch + 1], s1));
-            ADSB_CUDA(cudaMemcpyAsync(cursor_h + j, scal2 + 2 * j + 1, sizeof(unsigned long long),
-                                      cudaMemcpyDeviceToHost, s1));
-            ADSB_CUDA(cudaEventRecord(ev_sampled[j], s1));
-            sampled_frames += b.F;
-            L.count++;
-        };
-        int vbits = 1;
-        while (vbits < 32 && (1ull << vbits) < n) ++vbits;
-        const int end_bit = 32 + vbits;
-        Batch cur, nxt;
-        plan(cur, 0);
-        enqueue(cur);
-        bool have_next = plan(nxt, 1);
-        if (have_next) enqueue(nxt);
-        uint64_t done = 0;
-        bool stopped = false;
-        for (;;) {
-            const int j = cur.slot;
-            ADSB_CUDA(cudaEventSynchronize(ev_sampled[j]));
-            uint64_t E = cursor_h[j];
-            if (E > ctx.rt->pool.capacity<unsigned long long>(ev_id[j])) {
-                // event buffer overflow: redo this batch alone into a larger buffer
-                ADSB_CUDA(cudaStreamSynchronize(s1));
-                ADSB_CUDA(cudaStreamSynchronize(s2));
-                ev_buf[j] = ctx.rt->pool.get<unsigned long long>(ev_id[j], E + E / 4 + 1024);
-                slot_used[j] = false;
-                sampled_frames -= cur.F;
-                enqueue(cur);
-                ADSB_CUDA(cudaEventSynchronize(ev_sampled[j]));
-                E = cursor_h[j];
-            }
-            const uint64_t F = cur.F;
-            unsigned long long* ev = ev_buf[j];
-            unsigned long long* sorted = ctx.rt->pool.get<unsigned long long>(Scratch::kSorted, E);
-            uint32_t* frame_max = ctx.rt->pool.get<uint32_t>(Scratch::kFrameMax, F);
-            uint32_t* run_max = ctx.rt->pool.get<uint32_t>(Scratch::kRunMax, F);
-            size_t tb = 0, tb2 = 0;
-            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, ev, sorted, E, 0, end_bit, s2));
-            ADSB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb2, frame_max, run_max, MaxOp(),
-                                                     static_cast<int64_t>(F), s2));
-            tb = std::max(tb, tb2);
-            uint8_t* temp = ctx.rt->pool.get<uint8_t>(Scratch::kSortTemp, tb);
-            ADSB_CUDA(cudaStreamWaitEvent(s2, ev_sampled[j], 0));
-            ADSB_CUDA(cub::DeviceRadixSort::SortKeys(temp, tb, ev, sorted, E, 0, end_bit, s2));
-            ADSB_CUDA(cudaMemsetAsync(frame_max, 0, F * sizeof(uint32_t), s2));
-            k_event_values<<<grid_for(E, ctx.device), 256, 0, s2>>>(sorted, E, total, frame_max);
-            ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp, tb, frame_max, run_max, MaxOp(), static_cast<int64_t>(F), s2));
-            ADSB_CUDA(cudaMemsetAsync(stop_idx, 0xFF, sizeof(uint32_t), s2));
-            k_find_stop<<<grid_for(F, ctx.device), 256, 0, s2>>>(run_max, static_cast<uint32_t>(F), base_max, done,
-                                                                 spf, rule, stop_idx);
-            ADSB_CUDA(cudaMemcpyAsync(stop_h, stop_idx, sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
-            ADSB_CUDA(cudaStreamSynchronize(s2));
-            L.count += 3;
-            const uint32_t stop_host = *stop_h;
-            uint32_t limit = static_cast<uint32_t>(F - 1);
-            if (stop_host != kNoStop) {
-                limit = stop_host;
-                stopped = true;
-            } else if (done + F >= frame_limit) {
-                stopped = true;  // max_cycles cap
-                out.reason = ADSB_REASON_CAPPED;
-            }
-            k_apply<<<grid_for(E, ctx.device), 256, 0, s2>>>(ev, E, limit, total);
-            k_update_base<<<1, 32, 0, s2>>>(run_max, limit, base_max);
-            ADSB_CUDA(cudaEventRecord(ev_free[j], s2));
-            L.count += 2;
-            if (trace_enabled())
-                std::fprintf(stderr, "[adsb] det batch (pipelined): frames %llu..%llu events %llu stop %d t=%.3f ms\n",
-                             static_cast<unsigned long long>(done), static_cast<unsigned long long>(done + F),
-                             static_cast<unsigned long long>(E), stop_host == kNoStop ? -1 : static_cast<int>(stop_host),
-                             1e3 * ads.seconds());
-            if (stopped) {
-                done += static_cast<uint64_t>(limit) + 1;
-                break;
-            }
-            done += F;
-            if (!have_next) {  // cannot happen: the last batch reaches frame_limit and stops above
-                out.reason = ADSB_REASON_CAPPED;
-                break;
-            }
-            cur = nxt;
-            have_next = plan(nxt, 1 - cur.slot);
-            if (have_next) enqueue(nxt);
-        }
-        ADSB_CUDA(cudaStreamSynchronize(s1));  // a speculative batch may still be running
-        ADSB_CUDA(cudaStreamSynchronize(s2));
-        for (uint64_t i = 0; i < launches; ++i) {
-            float ms = 0;
-            ADSB_CUDA(cudaEventElapsedTime(&ms, ctx.rt->ev_launch[2 * i], ctx.rt->ev_launch[2 * i + 1]));
-            out.sampler_ms += ms;
-        }
-        out.total_samples = sampled_frames * spf;
-        out.check_cycles = done;
-        out.tau = done * spf;
-        out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
-    } else if (opt.deterministic) {
-        const uint64_t spf = opt.spf;
-        uint64_t frame_limit = (out.omega + spf - 1) / spf;  // the rule holds by tau >= omega
-        if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles);
-        frame_limit = std::max<uint64_t>(frame_limit, 1);
+        frame_limit = (frame_limit + C - 1) / C * C;           // epochs end on a multiple of B
+        if (opt.max_cycles) frame_limit = std::min(frame_limit, opt.max_cycles * C);
+        frame_limit = std::max<uint64_t>(frame_limit, C);
+        // bounded memory (engine.hpp:92, :137-144): at most a+1 frames ahead per team
+        const uint64_t bounded_cap =
+            opt.bounded_memory ? std::max<uint64_t>(teams * (opt.reservation_block + 1ull), C) : ~0ull;
         uint32_t* base_max = ctx.rt->pool.get<uint32_t>(Scratch::kBaseMax, 1);
         uint32_t* stop_idx = ctx.rt->pool.get<uint32_t>(Scratch::kStopIdx, 1);
         uint32_t* stop_h = reinterpret_cast<uint32_t*>(ctx.rt->pinned.ptr + kPinStop);
@@ -625,8 +511,11 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
                 F = std::min<uint64_t>(std::max<uint64_t>(need + need / 20 + 1, team_slots * world / 2),
                                        std::max<uint64_t>((growth - 1) * done, F));
             }
+            F = std::min<uint64_t>(F, bounded_cap);
+            F = (F + C - 1) / C * C;  // whole epochs
             F = std::min<uint64_t>(F, frame_limit - done);
-            F = std::min<uint64_t>(F, 1ull << 30);
+            F = std::min<uint64_t>(F, (1ull << 30) / C * C);
+            observe_depth(F);
             SamplerParams p = base_params(ctx, opt.seed, spf);
             p.first = done;
             p.rank = static_cast<uint32_t>(rank);
@@ -638,25 +527,20 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             adapt_store(ctx, stats, s1);
             unsigned long long* ev = events;
             uint64_t count = E;
-            if (opt.comm) {
+            if (world > 1) {
                 // gather every rank's events so each rank runs the identical cutoff
-                unsigned long long* dmax = ctx.rt->pool.get<unsigned long long>(Scratch::kNcclScalar, 1);
-                *emax_h = E;
-                ADSB_CUDA(cudaMemcpyAsync(dmax, emax_h, sizeof(unsigned long long), cudaMemcpyHostToDevice, s1));
-                ADSB_NCCL(ncclAllReduce(dmax, dmax, 1, ncclUint64, ncclMax, opt.comm->comm, s1));
-                ADSB_CUDA(cudaMemcpyAsync(emax_h, dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s1));
-                ADSB_CUDA(cudaStreamSynchronize(s1));
-                const unsigned long long emax = *emax_h;
+                uint64_t emax = E;
+                comm_allreduce_host(opt.comm, &emax, 1, RedOp::kMax, s1);
                 if (ctx.rt->pool.capacity<unsigned long long>(Scratch::kEvents) < emax) {
                     unsigned long long* tmp = ctx.rt->pool.get<unsigned long long>(Scratch::kSorted, E);
                     ADSB_CUDA(cudaMemcpyAsync(tmp, events, E * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s1));
                     events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, emax);
                     ADSB_CUDA(cudaMemcpyAsync(events, tmp, E * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s1));
                 }
-                if (emax > E)
+                if (emax > E)  // padding: all-ones keys sort last and are skipped
                     ADSB_CUDA(cudaMemsetAsync(events + E, 0xFF, (emax - E) * sizeof(unsigned long long), s1));
                 unsigned long long* gathered = ctx.rt->pool.get<unsigned long long>(Scratch::kGathered, emax * world);
-                ADSB_NCCL(ncclAllGather(events, gathered, emax, ncclUint64, opt.comm->comm, s1));
+                comm_allgather_u64(opt.comm, events, gathered, emax, s1);
                 ev = gathered;
                 count = emax * world;
             }
@@ -665,7 +549,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             uint32_t* frame_max = ctx.rt->pool.get<uint32_t>(Scratch::kFrameMax, F);
             uint32_t* run_max = ctx.rt->pool.get<uint32_t>(Scratch::kRunMax, F);
             int end_bit = 64;
-            if (!opt.comm) {
+            if (world == 1) {
                 int vbits = 1;
                 while (vbits < 32 && (1ull << vbits) < n) ++vbits;
                 end_bit = 32 + vbits;
@@ -682,7 +566,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             ADSB_CUDA(cub::DeviceScan::InclusiveScan(temp, tb, frame_max, run_max, MaxOp(), static_cast<int64_t>(F), s1));
             ADSB_CUDA(cudaMemsetAsync(stop_idx, 0xFF, sizeof(uint32_t), s1));
             k_find_stop<<<grid_for(F, ctx.device), 256, 0, s1>>>(run_max, static_cast<uint32_t>(F), base_max, done, spf,
-                                                                 rule, stop_idx);
+                                                                 C, rule, stop_idx);
             ADSB_CUDA(cudaMemcpyAsync(stop_h, stop_idx, sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
             ADSB_CUDA(cudaMemcpyAsync(stop_h + 1, run_max + (F - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s1));
             ADSB_CUDA(cudaStreamSynchronize(s1));
@@ -712,15 +596,20 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         }
         max_dev32 = base_max;  // k_update_base folded the running max up to the stop frame
         out.total_samples = sampled_frames * spf;
-        out.check_cycles = done;
         out.tau = done * spf;
-        out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
-    } else if (!opt.comm && arena(ctx).kind == 1 && !std::getenv("ADSB_NO_FUSED")) {
+        if (opt.deterministic) {
+            out.check_cycles = done;
+            out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
+        } else {
+            out.check_cycles = done / C;
+            out.stop_epoch = out.check_cycles;
+        }
+    } else if (fused_mode) {
         // ---- cumulative epochs, fused: one persistent launch folds finished
         // epochs in order and evaluates the rule on the device (no host round
         // trip per epoch), so epochs can be as small as the reference's check
         // interval and the run stops within ~K epochs + one sample per block.
-        const uint64_t B = opt.epoch_samples ? opt.epoch_samples : 1024;
+        const uint64_t B = epoch_B;
         uint64_t max_epochs = (out.omega + B - 1) / B;
         if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
         max_epochs = std::max<uint64_t>(max_epochs, 1);
@@ -731,6 +620,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         // profiles/r01_ab_round3.txt). Memory 8 B x K x n.
         uint32_t K = 32;
         if (const char* e = std::getenv("ADSB_RING_K")) K = std::min<uint32_t>(std::max<uint32_t>(std::strtoul(e, nullptr, 10), 2), 64);
+        observe_depth(static_cast<uint64_t>(K) * B);
         unsigned long long* ctl = ctx.rt->pool.get<unsigned long long>(Scratch::kCtl, kCtlWords);
         uint32_t* ring_cnt = ctx.rt->pool.get<uint32_t>(Scratch::kRingCnt, static_cast<size_t>(K) * n);
         uint32_t* ring_list = ctx.rt->pool.get<uint32_t>(Scratch::kRingList, static_cast<size_t>(K) * n);
@@ -793,12 +683,12 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
                          static_cast<unsigned long long>(B), static_cast<unsigned long long>(stop),
                          static_cast<unsigned long long>(out.total_samples), 1e3 * t_launch, 1e3 * ads.seconds());
     } else {
-        // ---- cumulative epoch pipeline
-        uint64_t B = opt.epoch_samples;
-        if (B == 0) {
-            B = std::max<uint64_t>(4 * team_slots * world, 1024);
-            B = std::min<uint64_t>(B, std::max<uint64_t>(out.omega / 4, 1024));
-        }
+        // ---- cumulative epochs as run_barrier rounds (engine.hpp:267-341): each
+        // round of B samples is split across the ranks; stream 2 all-reduces the
+        // round's n-length count vector, folds it and checks the rule while stream
+        // 1 samples the next round into the other buffer.
+        const uint64_t B = epoch_B;
+        observe_depth(2 * B);
         uint64_t max_epochs = (out.omega + B - 1) / B;
         if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
         max_epochs = std::max<uint64_t>(max_epochs, 1);
@@ -850,7 +740,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             const int k = static_cast<int>(e & 1);
             ADSB_CUDA(cudaStreamWaitEvent(s2, samp[k], 0));
             uint32_t* ec = cnt + static_cast<size_t>(k) * n;
-            if (opt.comm) ADSB_NCCL(ncclAllReduce(ec, ec, n, ncclUint32, ncclSum, opt.comm->comm, s2));
+            comm_allreduce_u32_sum(opt.comm, ec, n, s2);
             k_fold_epoch<<<grid_for(n, ctx.device), 256, 0, s2>>>(total, ec, n, dmax + k);
             k_epoch_rule<<<1, 32, 0, s2>>>(dmax + k, (e + 1) * B, rule, flag_dev + k);
             ADSB_CUDA(cudaMemcpyAsync(flag_host + k, flag_dev + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
@@ -917,6 +807,8 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
     out.store_fallbacks = st_host[kStatFallbacks];
     out.degenerate_steps = st_host[kStatDegenerate];
     out.kernel_launches = L.count;
+    out.queue_mean_depth = depth_obs ? depth_sum / static_cast<double>(depth_obs) : 0.0;
+    out.queue_high_water_exceeded = out.queue_max_depth > opt.queue_high_water;
     // kadabra.hpp:339-343
     if (out.reason != ADSB_REASON_CAPPED) {
         out.reason = ADSB_REASON_OMEGA_REACHED;

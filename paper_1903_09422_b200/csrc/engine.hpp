@@ -12,8 +12,13 @@ namespace adsb {
 
 struct EngineOptions {
     bool deterministic = true;     // indexed frames vs cumulative epochs
+    bool barrier = false;          // cumulative epochs as run_barrier rounds (dense count all-reduce on N GPUs)
     uint64_t spf = 1000;           // samples per frame (deterministic)
-    uint64_t epoch_samples = 0;    // samples per epoch over all ranks (0 = auto)
+    uint64_t epoch_samples = 0;    // samples per epoch over all ranks (0 = 1024; barrier: check_interval)
+    uint64_t check_interval = 1000;
+    bool bounded_memory = false;   // engine.hpp:92: cap frames ahead of the cutoff
+    uint32_t reservation_block = 4;
+    uint64_t queue_high_water = 64;
     uint64_t seed = 1;
     uint64_t max_cycles = 0;       // 0 = until the stopping rule
     uint32_t nominal_threads = 1;  // T for stop_epoch (engine.hpp:562)
@@ -33,6 +38,11 @@ struct EngineOutput {
     uint64_t edges_scanned = 0, vertices_expanded = 0, kernel_launches = 0;
     uint64_t rebuild_edges = 0, backtrack_edges = 0, store_fallbacks = 0, degenerate_steps = 0;
     double sampler_ms = 0;
+    // engine.hpp:156-161 QueueStats (per sampler team)
+    uint64_t queue_max_depth = 0, queue_allocated = 0;
+    double queue_mean_depth = 0;
+    bool queue_high_water_exceeded = false;
+    uint32_t world = 1;
 };
 
 // kadabra.hpp:41-53

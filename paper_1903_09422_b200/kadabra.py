@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._lib import DomainError, InvalidArgument, Stats, check, dblp, lib, u32p, u64p
-from .adsamp import EngineConfig, Graph, RunResult, Variant
+from .adsamp import EngineConfig, Graph, QueueStats, RunResult, Variant
 
 
 def allocate_deltas(n: int, delta: float) -> tuple[np.ndarray, np.ndarray]:
@@ -70,9 +70,8 @@ def to_string(r: StopReason) -> str:
 class BcResult:
     """kadabra.hpp:295-304, plus the device counters of the executed sampler.
 
-    `scores` (data[v] / tau, kadabra.hpp:334-337) is computed on first access
-    from the counts, the same IEEE division the C ABI performs; estimate_bc
-    does not materialise it in the timed call."""
+    `scores` (data[v] / tau, kadabra.hpp:334-337) are filled by the C ABI in
+    the estimate_bc call itself, as the reference returns them."""
     _scores: np.ndarray | None = field(default=None, repr=False)
     tau: int = 0
     reason: StopReason = StopReason.eps_converged
@@ -93,11 +92,7 @@ class BcResult:
 
     @property
     def scores(self) -> np.ndarray:
-        if self._scores is None:
-            data = self.run.data
-            self._scores = (data.astype(np.float64) / float(self.tau) if self.tau
-                            else np.zeros(len(data), dtype=np.float64))
-        return self._scores
+        return self._scores if self._scores is not None else np.zeros(len(self.run.data), dtype=np.float64)
 
 
 def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | None = None,
@@ -108,14 +103,17 @@ def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | N
     cfg.validate()
     n = g.num_vertices()
     counts = np.empty(max(n, 1), dtype=np.uint64)
+    scores = np.empty(max(n, 1), dtype=np.float64)
     st = Stats()
     c = cfg.to_c()
-    check(lib().adsb_estimate_bc(g.handle, epsilon, delta, C.byref(c), None,
+    check(lib().adsb_estimate_bc(g.handle, epsilon, delta, C.byref(c), scores.ctypes.data_as(dblp),
                                  counts.ctypes.data_as(u64p), C.byref(st)))
     run = RunResult(data=counts[:n], num=st.tau, total_samples=st.total_samples,
                     per_thread_samples=[st.total_samples], check_cycles=st.check_cycles,
-                    stop_epoch=st.stop_epoch)
-    return BcResult(tau=st.tau, reason=StopReason(st.reason), omega=st.omega,
+                    stop_epoch=st.stop_epoch,
+                    queue=QueueStats(st.queue_max_depth, st.queue_mean_depth, st.queue_allocated,
+                                     bool(st.queue_high_water_exceeded)))
+    return BcResult(_scores=scores[:n], tau=st.tau, reason=StopReason(st.reason), omega=st.omega,
                     diameter_bound=st.diameter_bound, preprocess_seconds=st.preprocess_seconds,
                     ads_seconds=st.ads_seconds, run=run, num_components=st.num_components,
                     edges_scanned=st.edges_scanned, vertices_expanded=st.vertices_expanded,

@@ -7,6 +7,7 @@ that traverses the graph is GPU-only and covered by test_gpu_parity.py.
 from __future__ import annotations
 
 import ctypes as C
+import json
 import re
 from pathlib import Path
 
@@ -29,12 +30,14 @@ def test_c_abi_exports_every_declared_symbol():
     missing = [name for name in sorted(declared) if not hasattr(lib, name)]
     assert not missing, missing
     assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
-    assert _lib.lib().adsb_abi_version() == 1
+    assert _lib.lib().adsb_abi_version() == 2
 
 
 def test_struct_layouts():
-    assert C.sizeof(_lib.Config) == 80
-    assert C.sizeof(_lib.Stats) == 136
+    """ctypes mirrors of adsb.h's structs match the C compiler's layout."""
+    assert C.sizeof(_lib.Config) == 96
+    assert C.sizeof(_lib.Stats) == 168
+    assert C.sizeof(_lib.HostCollectives) == 24
 
 
 @pytest.mark.parametrize("text,n,m,ids", PARSE_CASES)
@@ -235,3 +238,28 @@ def test_no_cpu_fallback_without_gpu():
         kadabra.estimate_bc(g, 0.1, 0.1, adsamp.EngineConfig(variant=adsamp.Variant.indexed))
     with pytest.raises(CudaError):
         adsamp.connected_components(g)
+
+
+def test_bench_reference_arm_loads_no_product_code():
+    """bench.py --impl reference times the compiled reference on a graph made by
+    oracle/gen.c: the process must not map libadsb.so, and its metric string
+    must equal the GPU arm's (the driver compares them verbatim)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, runpy, json, io, contextlib\n"
+        "sys.argv=['bench.py','--impl','reference','--config','c1_er','--steps','1','--warmup','3']\n"
+        "buf=io.StringIO()\n"
+        "with contextlib.redirect_stdout(buf):\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "line=json.loads(buf.getvalue().strip().splitlines()[-1])\n"
+        "print(json.dumps({'metric': line['metric'], 'kind': line['cpu_baseline']['kind'],\n"
+        "  'libadsb': 'libadsb' in open('/proc/self/maps').read()}))\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=str(ROOT), capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    assert got["libadsb"] is False
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_1903_09422_b200 import datasets
+    assert got["metric"] == bench.metric_name(datasets.CONFIGS["c1_er"])

@@ -282,6 +282,29 @@ def test_golden_runs(gold_graphs):
         assert oracle.fnv1a(r.counts) == run["counts_fnv1a"]
 
 
+def test_golden_runs_threaded_oracle(gold_graphs):
+    """or_estimate_bc_threads (frames sampled in parallel, folded in position
+    order: how tests/golden/make_fullsize.py computes the full-size goldens the
+    reference cannot produce) reproduces every reference golden run."""
+    meta, arrays = golden()
+    for run in meta["runs"]:
+        g = oracle.from_pairs(gold_graphs[run["graph"]][0])
+        r = oracle.estimate_bc(g, run["eps"], run["delta"], spf=run["spf"], seed=run["seed"],
+                               nominal_threads=run["threads"], threads=3)
+        assert (r.tau, r.check_cycles, r.stop_epoch, r.reason) == \
+               (run["tau"], run["check_cycles"], run["stop_epoch"], run["reason"]), run["key"]
+        np.testing.assert_array_equal(r.counts, arrays["counts:" + run["key"]])
+
+
+def test_golden_frames_threaded_oracle(gold_graphs):
+    meta, arrays = golden()
+    for fr in meta["frames"]:
+        g = oracle.from_pairs(gold_graphs[fr["graph"]][0])
+        got = oracle.sample_frames(g, fr["seed"], fr["spf"], fr["first"], fr["count"], threads=3)
+        assert [len(x) for x in got] == list(arrays["frames_len:" + fr["key"]])
+        np.testing.assert_array_equal(np.concatenate(got), arrays["frames_ids:" + fr["key"]])
+
+
 def test_golden_frames(gold_graphs):
     meta, arrays = golden()
     for fr in meta["frames"]:
@@ -354,3 +377,38 @@ def test_epoch_mode_is_indexed_prefix():
     for inc in oracle.sample_frames(g, 3, 1, 0, e.tau):
         np.add.at(want, inc, 1)
     np.testing.assert_array_equal(e.counts, want)
+
+
+@pytest.mark.parametrize("name", ["c1_er", "c2_rmat18", "c3_ba", "c4_grid"])
+def test_generators_match_product(name):
+    """oracle/gen.c (what bench.py's reference arm generates its graph with, so
+    that arm never loads libadsb.so) emits the product generators' exact edge
+    sequence, LCC included."""
+    w = datasets.CONFIGS[name]
+    np.testing.assert_array_equal(oracle.gen_pairs(w.kind, w.params), datasets.pairs(name))
+
+
+def test_generators_match_product_small():
+    cases = [("gnm", (300, 900, 5), datasets.gen_gnm), ("rmat", (10, 8, 0.57, 0.19, 0.19, 3), datasets.gen_rmat),
+             ("ba", (500, 3, 9), datasets.gen_ba), ("grid", (40, 30, 0.3, 2), datasets.gen_grid)]
+    for kind, params, fn in cases:
+        np.testing.assert_array_equal(oracle.gen_pairs(kind, params), fn(*params))
+    for kind, params, fn in cases:
+        if kind != "ba":
+            np.testing.assert_array_equal(oracle.gen_pairs(kind, params, lcc=False), fn(*params, lcc=False))
+
+
+def test_dense_edges_file_roundtrip(tmp_path):
+    """The --graph-bin input of ref_driver: first-appearance dense ids, i.e. the
+    ids parse_edge_list assigns (graph.hpp:98-123)."""
+    pairs = datasets.gen_rmat(9, 8, 0.57, 0.19, 0.19, 4)
+    path = tmp_path / "g.bin"
+    oracle.write_dense_edges(path, pairs)
+    raw = path.read_bytes()
+    n = int(np.frombuffer(raw, "<u4", 1, 0)[0])
+    m = int(np.frombuffer(raw, "<u8", 1, 4)[0])
+    dense = np.frombuffer(raw, "<u4", 2 * m, 12)
+    g = oracle.from_pairs(pairs)
+    assert n == g.n and m == pairs.shape[0] // 2
+    ids = g.original_ids
+    np.testing.assert_array_equal(ids[dense], pairs)
