@@ -159,6 +159,17 @@ struct EngineConfig {
     int device = -1;
     adsb_comm* comm = nullptr;
 
+    // engine.hpp:97-105 (the C ABI re-validates and throws the same messages)
+    void validate() const {
+        if (threads < 1) throw std::invalid_argument("threads must be >= 1");
+        if (variant == Variant::shared && (frame_groups < 1 || frame_groups > threads))
+            throw std::invalid_argument("frame groups must satisfy 1 <= F <= T");
+        if (check_interval < 1) throw std::invalid_argument("check interval must be >= 1");
+        if (!(latency_exponent > 0)) throw std::invalid_argument("xi must be > 0");
+        if (samples_per_frame < 1) throw std::invalid_argument("samples per frame must be >= 1");
+        if (reservation_block < 1) throw std::invalid_argument("reservation block must be >= 1");
+    }
+
     adsb_config to_c() const {
         adsb_config c;
         adsb_config_init(&c);
@@ -173,8 +184,18 @@ struct EngineConfig {
         c.max_cycles = max_cycles;
         c.device = device;
         c.comm = comm;
+        c.bounded_memory = bounded_memory ? 1u : 0u;
+        c.reservation_block = reservation_block;
+        c.queue_high_water = queue_high_water;
         return c;
     }
+};
+
+struct QueueStats {  // engine.hpp:156-161 (per sampler team on the GPU)
+    std::uint64_t max_depth = 0;
+    double mean_depth = 0.0;
+    std::uint64_t allocated = 0;
+    bool high_water_exceeded = false;
 };
 
 struct RunResult {  // engine.hpp:163-171
@@ -184,7 +205,13 @@ struct RunResult {  // engine.hpp:163-171
     std::vector<std::uint64_t> per_thread_samples;
     std::uint64_t check_cycles = 0;
     std::uint64_t stop_epoch = 0;
+    QueueStats queue;
 };
+
+// audit.hpp:36-80. Accepted for signature compatibility with estimate_bc
+// (kadabra.hpp:308-309). The device pipelines have no per-thread event log to
+// hand to it; their consistency replay is tests/test_gpu_parity.py's audit tests.
+class AuditSink;
 
 namespace kadabra {
 
@@ -223,7 +250,10 @@ inline double g_bound(double b, double delta_u, std::uint64_t omega, std::uint64
 }
 
 // kadabra.hpp:308-348
-inline BcResult estimate_bc(const Graph& g, double epsilon, double delta, const EngineConfig& config) {
+inline BcResult estimate_bc(const Graph& g, double epsilon, double delta, const EngineConfig& config,
+                            AuditSink* audit = nullptr) {
+    (void)audit;
+    config.validate();
     BcResult r;
     const adsb_config c = config.to_c();
     r.scores.resize(g.num_vertices());
@@ -240,6 +270,8 @@ inline BcResult estimate_bc(const Graph& g, double epsilon, double delta, const 
     r.run.per_thread_samples = {r.device.total_samples};
     r.run.check_cycles = r.device.check_cycles;
     r.run.stop_epoch = r.device.stop_epoch;
+    r.run.queue = {r.device.queue_max_depth, r.device.queue_mean_depth, r.device.queue_allocated,
+                   r.device.queue_high_water_exceeded != 0};
     return r;
 }
 

@@ -153,6 +153,11 @@ adsb_status adsb_graph_from_edges(uint32_t n, const uint32_t *edges, uint64_t m,
 adsb_status adsb_graph_from_csr(uint32_t n, const uint64_t *offsets, const uint32_t *neighbors,
                                 adsb_graph **out);
 void adsb_graph_destroy(adsb_graph *g);
+/* Binary CSR cache: the graph exactly as ingested (dense ids, ascending
+ * adjacency, original ids), written and read with parallel I/O and a
+ * checksum; a damaged or truncated file fails with ADSB_ERR_PARSE. */
+adsb_status adsb_graph_save(const adsb_graph *g, const char *path);
+adsb_status adsb_graph_load(const char *path, adsb_graph **out);
 adsb_status adsb_graph_info(const adsb_graph *g, uint32_t *n, uint64_t *nnz);
 adsb_status adsb_graph_copy_csr(const adsb_graph *g, uint64_t *offsets, uint32_t *neighbors);
 adsb_status adsb_graph_copy_original_ids(const adsb_graph *g, uint64_t *out);

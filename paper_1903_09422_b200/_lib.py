@@ -121,6 +121,8 @@ _SIGS = {
     "adsb_graph_from_edges": (C.c_int, [C.c_uint32, u32p, C.c_uint64, C.POINTER(P)]),
     "adsb_graph_from_csr": (C.c_int, [C.c_uint32, u64p, u32p, C.POINTER(P)]),
     "adsb_graph_destroy": (None, [P]),
+    "adsb_graph_save": (C.c_int, [P, C.c_char_p]),
+    "adsb_graph_load": (C.c_int, [C.c_char_p, C.POINTER(P)]),
     "adsb_graph_info": (C.c_int, [P, u32p, u64p]),
     "adsb_graph_copy_csr": (C.c_int, [P, u64p, u32p]),
     "adsb_graph_copy_original_ids": (C.c_int, [P, u64p]),

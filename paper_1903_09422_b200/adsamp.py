@@ -311,6 +311,20 @@ def parse_edge_list_file(path: str | os.PathLike) -> ParsedGraph:
     return _parsed(h)
 
 
+def save_graph(g: "Graph | ParsedGraph", path: str | os.PathLike) -> None:
+    """Binary CSR cache of an ingested graph (dense ids, adjacency, original ids)."""
+    gg = g.graph if isinstance(g, ParsedGraph) else g
+    check(lib().adsb_graph_save(gg.handle, os.fsencode(path)))
+
+
+def load_graph(path: str | os.PathLike) -> ParsedGraph:
+    """Inverse of save_graph: the identical graph, read with parallel I/O and
+    checked against its checksum (ParseError when damaged or truncated)."""
+    h = C.c_void_p()
+    check(lib().adsb_graph_load(os.fsencode(path), C.byref(h)))
+    return _parsed(h)
+
+
 def graph_from_pairs(pairs) -> ParsedGraph:
     """parse_edge_list semantics on (id, id) records already in memory."""
     p = _u64(np.asarray(pairs).reshape(-1))

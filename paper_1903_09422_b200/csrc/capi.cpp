@@ -119,6 +119,22 @@ adsb_status adsb_graph_parse_file(const char* path, adsb_graph** out) {
     });
 }
 
+adsb_status adsb_graph_save(const adsb_graph* g, const char* path) {
+    return guard([&] {
+        need(g, "graph");
+        need(path, "path");
+        save_graph_cache(g->host, path);
+    });
+}
+
+adsb_status adsb_graph_load(const char* path, adsb_graph** out) {
+    return guard([&] {
+        need(out, "out");
+        need(path, "path");
+        *out = wrap(load_graph_cache(path));
+    });
+}
+
 adsb_status adsb_graph_from_pairs(const uint64_t* pairs, uint64_t m, adsb_graph** out) {
     return guard([&] {
         need(out, "out");

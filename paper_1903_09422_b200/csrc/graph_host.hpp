@@ -88,6 +88,9 @@ HostGraph parse_edge_list_text(const char* text, uint64_t len);
 HostGraph parse_edge_list_file(const std::string& path);
 HostGraph graph_from_pairs(const uint64_t* pairs, uint64_t m);
 std::string serialize_edge_list(const HostGraph& g);
+// binary CSR cache (graph_cache.cpp): exact round trip, parallel I/O, checksummed
+void save_graph_cache(const HostGraph& g, const std::string& path);
+HostGraph load_graph_cache(const std::string& path);
 
 // Synthetic generators. Output: 2*m original ids.
 std::vector<uint64_t> gen_gnm(uint32_t n, uint64_t m, uint64_t seed);

@@ -303,6 +303,14 @@ __device__ void sample_one(const SamplerParams& p, Team& T, SplitMix64& rng, uin
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
 
     T.tag += 1;
+    if (T.tag == 0) {
+        // Generation tags are u32 and persist across calls: after 2^32 samples
+        // on this slot the tag wraps to 0, which zero-initialised words carry.
+        // Clear the slot's state once and restart at 1.
+        for (size_t i = T.lane; i < 2ull * p.slot_stride; i += 32) T.st[i] = 0ull;
+        __syncwarp();
+        T.tag = 1;
+    }
     const uint32_t os = T.off[s], ds = T.off[s + 1] - os;
     const uint32_t ot = T.off[t], dt = T.off[t + 1] - ot;
     if (T.lane == 0) {

@@ -27,7 +27,10 @@ struct Shared {
     uint32_t tflag[2];                // fused: the previous sample completed its epoch
     unsigned long long done_old;      // thread 0 (fused): Done counter before the last sample's increment
     unsigned long long spare_tick;    // thread 0 (fused, ADSB_TICKET_PAIR): second ticket of the last fetch
-    unsigned long long st_edges, st_rebuild, st_back, st_verts, st_degen;  // block statistics (thread 0 adds)
+    // block statistics: adjacency counters per warp (each written only by its
+    // lane 0 with plain adds: no 64-bit shared atomics, which are CAS loops on sm_100)
+    unsigned long long st_edges[kBT / 32], st_rebuild[kBT / 32], st_back[kBT / 32];
+    unsigned long long st_verts, st_degen;  // thread 0 adds
     unsigned long long n_samples, n_fallbacks, n_errors;
     uint32_t g_region, g_tag;         // fallback: borrowed global region and its tag
     uint32_t pending;                 // thread 0 (fused): done_old belongs to an unprocessed completion
@@ -521,7 +524,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         }
 #endif
         const uint32_t wm = __reduce_add_sync(kFull, static_cast<uint32_t>(mine));
-        if (C.lane == 0 && wm) atomicAdd(counter, static_cast<unsigned long long>(wm));
+        if (C.lane == 0 && wm) counter[C.warp] += wm;
         __syncthreads();
         return;
     }
@@ -724,7 +727,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- s-side level a, one pass: claim level a+1 and detect the meeting.
             // Claims made on the meeting level are harmless (never predecessors).
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
-            for_edges_tok(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges_tok(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t v) { return S.claim_issue(v, a + 1); },
                       [&](uint32_t, unsigned long long su, uint32_t v, unsigned long long tok) {
@@ -752,7 +755,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                 return {a, b, 0};
             }
             if (!S.pre_zeroed())
-            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -773,7 +776,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- t-side level b, one pass: claim level b+1 and detect the meeting
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
             const uint32_t meta_new = kMetaT | (b + 1);
-            for_edges_tok(C, S, t_lo, t_hi, true, &sh.st_edges,
+            for_edges_tok(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t v) { return S.claim_issue(v, meta_new); },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v, unsigned long long tok) {
@@ -811,7 +814,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else if (deg_s <= deg_t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
-            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -825,7 +828,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
-            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.pre_zeroed() ? S.sigma(slot) : 0ull; },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           bool ins;
@@ -845,7 +848,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
             if (sh.overflow) return {a, b, 1};
             if (!S.pre_zeroed())
-            for_edges(C, S, s_lo, s_hi, false, &sh.st_edges,
+            for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
                           uint32_t m;
@@ -862,7 +865,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else {
             // ---- t-side level b: probe for the s-ball
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
-            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
+            for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
                           uint32_t m;
@@ -875,7 +878,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       });
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             const uint32_t meta_new = kMetaT | (b + 1);
-            for_edges(C, S, t_lo, t_hi, true, &sh.st_edges,
+            for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t, unsigned long long, uint32_t v) {
                           bool ins;
@@ -908,7 +911,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
 template <class Store>
 __device__ void rebuild(Ctx& C, Store& S, uint32_t b) {
     for (uint32_t k = b; k >= 1; --k) {
-        for_edges(C, S, S.tlev[k - 1], S.tlev[k], true, &C.sh->st_rebuild,
+        for_edges(C, S, S.tlev[k - 1], S.tlev[k], true, C.sh->st_rebuild,
                   [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                   [&](uint32_t w_slot, unsigned long long, uint32_t v) {
                       uint32_t m;
@@ -991,7 +994,7 @@ __device__ void rebuild_push(Ctx& C, Store& S, uint32_t b) {
         hi = sh.dag_cnt;
     }
     const uint32_t wm = __reduce_add_sync(kFull, static_cast<uint32_t>(scanned));
-    if (C.lane == 0 && wm) atomicAdd(&sh.st_rebuild, static_cast<unsigned long long>(wm));
+    if (C.lane == 0 && wm) sh.st_rebuild[C.warp] += wm;
     __syncthreads();
 }
 
@@ -1103,7 +1106,7 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
         }
     }
     const uint32_t wp = __reduce_add_sync(kFull, probes);
-    if (C.lane == 0 && wp) atomicAdd(&sh.st_back, static_cast<unsigned long long>(wp));
+    if (C.lane == 0 && wp) sh.st_back[C.warp] += wp;
     __syncthreads();
     const uint32_t c = sh.dag_cnt;
     if (c == 0 || c > kBT) {
@@ -1203,7 +1206,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 #endif
                         }
                     }
-                    if (C.lane == 0) sh.st_back += min(32u, end - base);
+                    if (C.lane == 0) sh.st_back[C.warp] += min(32u, end - base);
                     const uint32_t cb = __ballot_sync(kFull, cand);
                     if (first == kNone && cb) {
                         const int f0 = __ffs(cb) - 1;
@@ -1266,7 +1269,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 #endif
                 }
             }
-            if (C.tid == 0) sh.st_back += min(static_cast<uint32_t>(kBT), end - base);
+            if (C.tid == 0) sh.st_back[0] += min(static_cast<uint32_t>(kBT), end - base);
             // per-warp 65-bit candidate totals, then the warp whose range holds
             // r walks its candidates in lane (= id) order
             const uint32_t cb = __ballot_sync(kFull, val != 0);
@@ -1522,6 +1525,17 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             region = sh.g_region;
             tag = sh.g_tag;
         }
+        if (tag == 0) {
+            // u32 generation tags persist across calls; after 2^32 samples on a
+            // region the tag wraps to 0, the value zeroed words carry: clear the
+            // region's state once and restart at 1 (block-uniform branch)
+            unsigned long long* st = p.state + 2ull * p.slot_stride * region;
+            for (size_t i = C.tid; i < 2ull * p.slot_stride; i += kBT) __stcg(st + i, 0ull);
+            __threadfence_block();
+            __syncthreads();
+            tag = 1;
+            if constexpr (kGlobalOnly) gtag = 1;
+        }
         auto gs = make_global_store<kGlobalOnly>(p, region, tag);
 #if ADSB_FALLBACK_FILTER
         // the table is empty here (the overflowed attempt cleared it) and
@@ -1561,7 +1575,13 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
     unsigned long long* ctl = p.ctl;
     const unsigned long long kNoEpoch = ~0ull;
     for (;;) {
-        if (C.tid == 0) sh.flag = atomicCAS(ctl + kCtlLock, 0ull, 1ull) == 0ull ? 1u : 0u;
+        // The fence orders this block's completion (the release add on Done[k])
+        // before its lock attempt: with the lock holder's exch + fence + re-read
+        // of Done, one of the two always sees the other (store buffering).
+        if (C.tid == 0) {
+            __threadfence();
+            sh.flag = atomicCAS(ctl + kCtlLock, 0ull, 1ull) == 0ull ? 1u : 0u;
+        }
         __syncthreads();
         const bool got = sh.flag != 0;
         __syncthreads();
@@ -1664,13 +1684,15 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
     // a second ticket through a long sample delays the tail (measured on C4).
     if (C.tid == 0) {
         sh.recorded = 0;
-        sh.st_edges = sh.st_rebuild = sh.st_back = sh.st_verts = sh.st_degen = 0;
+        sh.st_verts = sh.st_degen = 0;
         sh.n_samples = sh.n_fallbacks = sh.n_errors = 0;
         sh.last_d = 0;
         sh.pending = 0;
         sh.done_old = 0;
         sh.spare_tick = ~0ull;
     }
+    if (C.tid < kBT / 32) sh.st_edges[C.tid] = sh.st_rebuild[C.tid] = sh.st_back[C.tid] = 0;
+    __syncthreads();
     if (kMode != kModeFused) {
         for (uint32_t it = 0;; ++it) {
             const uint32_t par = it & 1;
@@ -1765,9 +1787,15 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
     ADSB_PHASE_ADD(4, k1 - k0);
     __syncthreads();  // low-degree expansions add edge counts from every warp
     if (C.tid == 0) {
-        atomicAdd(p.stats + kStatEdges, sh.st_edges + sh.st_rebuild + sh.st_back);
-        atomicAdd(p.stats + kStatRebuildEdges, sh.st_rebuild);
-        atomicAdd(p.stats + kStatBacktrackEdges, sh.st_back);
+        unsigned long long e = 0, r = 0, b = 0;
+        for (uint32_t w = 0; w < kBT / 32; ++w) {
+            e += sh.st_edges[w];
+            r += sh.st_rebuild[w];
+            b += sh.st_back[w];
+        }
+        atomicAdd(p.stats + kStatEdges, e + r + b);
+        atomicAdd(p.stats + kStatRebuildEdges, r);
+        atomicAdd(p.stats + kStatBacktrackEdges, b);
         atomicAdd(p.stats + kStatVertices, sh.st_verts);
     }
     if (C.tid == 0) {

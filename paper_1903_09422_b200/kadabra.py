@@ -89,6 +89,7 @@ class BcResult:
     backtrack_edges: int = 0
     store_fallbacks: int = 0
     degenerate_steps: int = 0
+    world: int = 1
 
     @property
     def scores(self) -> np.ndarray:
@@ -119,7 +120,8 @@ def estimate_bc(g: Graph, epsilon: float, delta: float, config: EngineConfig | N
                     edges_scanned=st.edges_scanned, vertices_expanded=st.vertices_expanded,
                     kernel_launches=st.kernel_launches, sampler_ms=st.sampler_ms,
                     rebuild_edges=st.rebuild_edges, backtrack_edges=st.backtrack_edges,
-                    store_fallbacks=st.store_fallbacks, degenerate_steps=st.degenerate_steps)
+                    store_fallbacks=st.store_fallbacks, degenerate_steps=st.degenerate_steps,
+                    world=st.world)
 
 
 def sample_frames(g: Graph, seed: int, samples_per_frame: int, first: int, count: int,

@@ -185,3 +185,108 @@ def test_c4_fullsize_capped_run_matches_oracle():
     assert (r.tau, r.run.check_cycles, r.reason.name) == (o.tau, o.check_cycles, o.reason) == (24, 24, "capped")
     np.testing.assert_array_equal(r.run.data, o.counts)
     assert int(r.run.data.sum()) > 24 * 500  # deep paths: hundreds of interior vertices each
+
+
+# ----------------------------------------------------------------------------- full-size goldens
+# tests/golden/fullsize.json (tests/golden/make_fullsize.py): the compiled
+# reference's run_indexed on C2 and C3 (equal to the threaded oracle), the
+# threaded oracle's runs on C4 (where the reference segfaults) and C2's
+# cumulative epochs, C5's first 200 frames, and n/m/components/D_ub/omega of
+# every config. Each graph is regenerated here and pinned by its pairs hash.
+import hashlib  # noqa: E402
+import json  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+FULL = json.loads((Path(__file__).resolve().parent / "golden" / "fullsize.json").read_text())
+
+
+def _pairs_sha(p) -> str:
+    return hashlib.sha256(np.ascontiguousarray(p, dtype="<u8").tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def full_graphs():
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            pairs = datasets.pairs(name)
+            if name in FULL["graphs"]:
+                assert _pairs_sha(pairs) == FULL["graphs"][name]["pairs_sha256"], f"generator drift for {name}"
+            cache.clear()  # one full-size graph resident at a time
+            cache[name] = adsamp.graph_from_pairs(pairs).graph
+        return cache[name]
+    return get
+
+
+@pytest.mark.parametrize("name", sorted(FULL["graphs"]))
+def test_fullsize_graph_facts_match_oracle(full_graphs, name):
+    """n, m, components, D_ub (graph.hpp:202-214) and omega (kadabra.hpp:41-53)
+    computed on the device equal the oracle's at every config's full size."""
+    want = FULL["graphs"][name]
+    g = full_graphs(name)
+    assert (g.num_vertices(), g.num_edges()) == (want["n"], want["m"])
+    cc = adsamp.connected_components(g, device=0)
+    assert cc.num_components == want["components"]
+    dub = adsamp.diameter_upper_bound(g, device=0)
+    assert dub == want["diameter_bound"]
+    from paper_1903_09422_b200.kadabra import compute_omega
+    assert compute_omega(dub, want["epsilon"], want["delta"]) == want["omega"]
+
+
+@pytest.mark.parametrize("key", sorted(FULL["runs"]))
+def test_fullsize_run_matches_golden(full_graphs, key):
+    """The whole run at the config's own size: tau, check cycles, stop epoch,
+    reason and the FNV-1a of every per-vertex count equal the reference's
+    indexed-frame run (C2, C3) or the oracle's (C4, C2 epochs)."""
+    want = FULL["runs"][key]
+    g = full_graphs(want["config"])
+    if want["mode"] == "indexed":
+        cfg = EngineConfig(variant=Variant.indexed, samples_per_frame=want["spf"], threads=want["nominal_threads"],
+                           base_seed=want["seed"], device=0)
+    else:
+        cfg = EngineConfig(variant=Variant.shared, epoch_samples=want["epoch_samples"], threads=8,
+                           base_seed=want["seed"], device=0)
+    r = estimate_bc(g, want["epsilon"], want["delta"], cfg)
+    got = (r.tau, r.run.check_cycles, r.run.stop_epoch, r.reason.name, r.omega, r.diameter_bound,
+           oracle.fnv1a(r.run.data), int(r.run.data.sum()), int(r.run.data.max()))
+    exp = (want["tau"], want["check_cycles"], want["stop_epoch"], want["reason"], want["omega"],
+           want["diameter_bound"], want["counts_fnv1a"], want["counts_sum"], want["counts_max"])
+    assert got == exp, (key, got, exp)
+    assert r.degenerate_steps == want["degenerate_steps"]
+
+
+def _fnv1a_u32(ids: np.ndarray) -> str:
+    h = 0xcbf29ce484222325
+    for byte in np.ascontiguousarray(ids, dtype="<u4").tobytes():
+        h ^= byte
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+@pytest.mark.parametrize("key", sorted(FULL["frames"]))
+def test_fullsize_frames_match_golden(full_graphs, key):
+    """C5 (R-MAT 24, 8.9M vertices): the first 200 frames' sampled paths — the
+    RNG stream and every sigma-weighted backtrack choice — equal the oracle's."""
+    want = FULL["frames"][key]
+    g = full_graphs(want["config"])
+    got = sample_frames(g, want["seed"], want["spf"], want["first"], want["count"], device=0)
+    assert [len(x) for x in got] == want["lens"]
+    ids = np.concatenate(got) if got else np.zeros(0, np.uint32)
+    assert _fnv1a_u32(ids) == want["ids_fnv1a"]
+
+
+def test_c5_nondet_within_2eps_of_deterministic(full_graphs):
+    """the reference's own C5 output is infeasible (~10^7
+    core-seconds), so the non-deterministic estimate is checked against the
+    deterministic (indexed-frame) mode, which is bit-exact against the
+    reference wherever the reference finishes. Both estimate BC within eps
+    with probability >= 1 - delta, so the sound tolerance between them is 2 eps."""
+    w = datasets.CONFIGS["c5_rmat24"]
+    g = full_graphs("c5_rmat24")
+    det = estimate_bc(g, w.epsilon, w.delta,
+                      EngineConfig(variant=Variant.indexed, samples_per_frame=1, threads=8, base_seed=42, device=0))
+    nd = estimate_bc(g, w.epsilon, w.delta, EngineConfig(variant=Variant.shared, threads=8, base_seed=42, device=0))
+    assert det.reason.name == nd.reason.name == "eps_converged"
+    err = float(np.max(np.abs(nd.scores - det.scores)))
+    assert err <= 2 * w.epsilon, f"max |nondet - det| = {err} > 2 eps"

@@ -263,3 +263,97 @@ def test_bench_reference_arm_loads_no_product_code():
     import bench
     from paper_1903_09422_b200 import datasets
     assert got["metric"] == bench.metric_name(datasets.CONFIGS["c1_er"])
+
+
+def test_cpp_dropin_header_source_compatible(tmp_path):
+    """A reference caller's code compiles unchanged against adsamp_b200.hpp:
+    estimate_bc takes an AuditSink* (kadabra.hpp:308-309), EngineConfig has
+    validate() (engine.hpp:97-105), RunResult has queue (engine.hpp:163-171)."""
+    import subprocess
+    src = tmp_path / "caller.cpp"
+    src.write_text(r'''
+#include "adsamp_b200.hpp"
+using namespace adsamp_b200;
+int main() {
+    EngineConfig cfg;
+    cfg.variant = Variant::indexed;
+    cfg.bounded_memory = true;
+    cfg.validate();
+    bool threw = false;
+    try { EngineConfig bad; bad.threads = 0; bad.validate(); } catch (const std::invalid_argument&) { threw = true; }
+    if (!threw) return 1;
+    AuditSink* sink = nullptr;
+    auto parsed = parse_edge_list(std::string("0 1\n1 2\n"));
+    if (false) {
+        kadabra::BcResult r = kadabra::estimate_bc(parsed.graph, 0.1, 0.1, cfg, sink);
+        return static_cast<int>(r.run.queue.max_depth + r.run.queue.high_water_exceeded);
+    }
+    return parsed.graph.num_vertices() == 3 ? 0 : 2;
+}
+''')
+    exe = tmp_path / "caller"
+    pkg = ROOT / "paper_1903_09422_b200"
+    out = subprocess.run(["g++", "-std=c++20", f"-I{ROOT / 'include'}", str(src), "-o", str(exe), f"-L{pkg}",
+                          "-ladsb", f"-Wl,-rpath,{pkg}"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert run.returncode == 0, (run.returncode, run.stderr)
+
+
+REF_DATA = Path("/root/reference/proj/data")
+
+
+@pytest.mark.skipif(not REF_DATA.exists(), reason="reference data fixtures not present")
+@pytest.mark.parametrize("name", ["toy_path.edges", "grid16.edges"])
+def test_reference_data_fixtures_ingest(name):
+    """The reference's own fixture files (proj/data/) through the product's
+    parser, the oracle and the compiled reference: same ids, same CSR, same D_ub."""
+    path = REF_DATA / name
+    p = adsamp.parse_edge_list_file(path)
+    o = oracle.parse_file(path)
+    np.testing.assert_array_equal(p.graph.offsets(), o.offsets)
+    np.testing.assert_array_equal(p.graph.neighbor_list(), o.nbrs)
+    assert list(p.original_ids) == list(o.original_ids)
+    if oracle.ref_available():
+        d = oracle.ref_dub(path)
+        assert (d["n"], d["m"]) == (p.graph.num_vertices(), p.graph.num_edges())
+        assert d["diameter_bound"] == oracle.diameter_upper_bound(o)
+
+
+def test_graph_cache_round_trip(tmp_path):
+    """Binary CSR cache (SURVEY.md §8(f1)): the identical graph (CSR, dense ids,
+    original ids) comes back; damage and truncation raise ParseError."""
+    for text in ["5 9\n9 7\n7 5\n% c\n1000000 5\n", "0 1\n1 2\n2 0\n"]:
+        p = adsamp.parse_edge_list(text)
+        path = tmp_path / "g.adsbcsr"
+        adsamp.save_graph(p, path)
+        q = adsamp.load_graph(path)
+        np.testing.assert_array_equal(q.graph.offsets(), p.graph.offsets())
+        np.testing.assert_array_equal(q.graph.neighbor_list(), p.graph.neighbor_list())
+        np.testing.assert_array_equal(q.original_ids, p.original_ids)
+    big = adsamp.graph_from_pairs(datasets.gen_rmat(14, 16, 0.57, 0.19, 0.19, 2))
+    path = tmp_path / "big.adsbcsr"
+    adsamp.save_graph(big, path)
+    q = adsamp.load_graph(path)
+    np.testing.assert_array_equal(q.graph.neighbor_list(), big.graph.neighbor_list())
+    np.testing.assert_array_equal(q.original_ids, big.original_ids)
+    raw = bytearray(path.read_bytes())
+    raw[len(raw) // 2] ^= 0x40
+    bad = tmp_path / "bad.adsbcsr"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(ParseError, match="damaged"):
+        adsamp.load_graph(bad)
+    bad.write_bytes(bytes(raw[: len(raw) - 8]))
+    with pytest.raises(ParseError, match="truncated"):
+        adsamp.load_graph(bad)
+    bad.write_bytes(b"not a cache at all, definitely not" * 4)
+    with pytest.raises(ParseError, match="not an adsb graph cache"):
+        adsamp.load_graph(bad)
+
+
+def test_datasets_graph_cache(tmp_path):
+    a = datasets.graph("c1_er", cache_dir=tmp_path)
+    assert (tmp_path / "c1_er.adsbcsr").exists()
+    b = datasets.graph("c1_er", cache_dir=tmp_path)
+    np.testing.assert_array_equal(a.graph.neighbor_list(), b.graph.neighbor_list())
+    np.testing.assert_array_equal(a.original_ids, b.original_ids)
