@@ -20,8 +20,11 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OBJ = ROOT / "build" / "obj"
-LIB = PKG / "libadsb.so"
+# ADSB_BUILD_TAG=<tag>: an A/B variant (with ADSB_NVCC_EXTRA flags) built into
+# build/obj_<tag> and ab/libadsb_<tag>.so, loaded with ADSB_LIB_PATH
+_TAG = os.environ.get("ADSB_BUILD_TAG", "")
+OBJ = ROOT / "build" / (f"obj_{_TAG}" if _TAG else "obj")
+LIB = (ROOT / "ab" / f"libadsb_{_TAG}.so") if _TAG else PKG / "libadsb.so"
 TOOL = PKG / "adsb_run"
 TOOL_SRC = ROOT / "tools" / "adsb_run.cpp"
 
@@ -62,6 +65,7 @@ def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
+    LIB.parent.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
     newest_header = max((h.stat().st_mtime for h in _headers()), default=0.0)
     todo = []
@@ -80,7 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}\n{res.stdout}")
-    if TOOL_SRC.exists() and (not TOOL.exists() or TOOL.stat().st_mtime < max(LIB.stat().st_mtime,
+    if not _TAG and TOOL_SRC.exists() and (not TOOL.exists() or TOOL.stat().st_mtime < max(LIB.stat().st_mtime,
                                                                             TOOL_SRC.stat().st_mtime)):
         cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++20", f"-I{ROOT / 'include'}", str(TOOL_SRC),
                "-o", str(TOOL), f"-L{PKG}", "-ladsb", "-Wl,-rpath,$ORIGIN"]

@@ -280,6 +280,10 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
         const uint64_t csr = 4ull * (ctx.graph.n + 1) + 4ull * ctx.graph.nnz;
         p.csr_hint = csr * 2 <= static_cast<uint64_t>(l2) ? 1.0f : 0.0f;
         if (const char* e = std::getenv("ADSB_CSR_HINT")) p.csr_hint = std::strtof(e, nullptr);
+        // vectorised adjacency reads where the CSR misses L2 (C5: -1%); on an
+        // L2-resident CSR the scalar loop is faster (C2 -7%, C3 -10%)
+        p.vec4 = csr > static_cast<uint64_t>(l2) ? 1u : 0u;
+        if (const char* e = std::getenv("ADSB_VEC4")) p.vec4 = std::strtoul(e, nullptr, 10) ? 1u : 0u;
     }
     p.dagq = a.dagq.ptr;
     p.slot_tag = a.slot_tag.ptr;
@@ -374,6 +378,42 @@ bool trace_enabled() {
     static const bool on = std::getenv("ADSB_TRACE") != nullptr;
     return on;
 }
+
+bool rule_passes_host(uint64_t max_count, uint64_t tau, const RuleParams& r) {
+    return tau >= r.omega || converged_at_max(max_count, tau, r.omega, r.eps, r.log_inv);
+}
+
+// ADSB_AUDIT=<file>: a validate_consistency-style log (audit.hpp:101-161
+// analogue, diagnostics only) of the host-orchestrated pipelines, replayed by
+// tests/test_gpu_parity.py: per frame batch its first frame, size, the
+// running max after every frame (the check record) and every increment
+// event; per barrier round the all-reduced round counts and the check.
+// u64 records:  [1, first, F, events, limit, stopped, base_max] run_max[F] events[events]
+//               [2, epoch, B, pass, max] counts[n]
+//               [3, tau, check_cycles]
+struct AuditLog {
+    FILE* f = nullptr;
+    AuditLog() {
+        if (const char* path = std::getenv("ADSB_AUDIT")) f = std::fopen(path, "wb");
+    }
+    ~AuditLog() {
+        if (f) std::fclose(f);
+    }
+    explicit operator bool() const { return f != nullptr; }
+    void words(std::initializer_list<uint64_t> w) {
+        for (uint64_t x : w) std::fwrite(&x, 8, 1, f);
+    }
+    template <class T>
+    void device_array(const T* dev, uint64_t count, cudaStream_t s) {
+        std::vector<T> h(count);
+        if (count) ADSB_CUDA(cudaMemcpyAsync(h.data(), dev, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+        ADSB_CUDA(cudaStreamSynchronize(s));
+        for (T x : h) {
+            const uint64_t w = static_cast<uint64_t>(x);
+            std::fwrite(&w, 8, 1, f);
+        }
+    }
+};
 
 }  // namespace
 
@@ -492,6 +532,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         unsigned long long* emax_h = ctx.rt->pinned.ptr + kPinEmax;
         ADSB_CUDA(cudaMemsetAsync(base_max, 0, sizeof(uint32_t), s1));
         unsigned long long* events = ctx.rt->pool.get<unsigned long long>(Scratch::kEvents, 1 << 20);
+        AuditLog audit;
         uint64_t done = 0;  // frames folded so far
         uint64_t sampled_frames = 0;
         bool stopped = false;
@@ -583,6 +624,14 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
                 stop_local = limit;
                 out.reason = ADSB_REASON_CAPPED;
             }
+            if (audit) {
+                uint32_t bm = 0;
+                ADSB_CUDA(cudaMemcpyAsync(&bm, base_max, sizeof bm, cudaMemcpyDeviceToHost, s1));
+                ADSB_CUDA(cudaStreamSynchronize(s1));
+                audit.words({1, done, F, count, limit, stopped ? 1u : 0u, bm});
+                audit.device_array(run_max, F, s1);
+                audit.device_array(ev, count, s1);
+            }
             k_apply<<<grid_for(count, ctx.device), 256, 0, s1>>>(ev, count, limit, total);
             k_update_base<<<1, 32, 0, s1>>>(run_max, limit, base_max);
             L.count += 2;
@@ -597,6 +646,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         max_dev32 = base_max;  // k_update_base folded the running max up to the stop frame
         out.total_samples = sampled_frames * spf;
         out.tau = done * spf;
+        if (audit) audit.words({3, done * spf, opt.deterministic ? done : done / C});
         if (opt.deterministic) {
             out.check_cycles = done;
             out.stop_epoch = (done - 1) / std::max<uint32_t>(opt.nominal_threads, 1) + 1;  // engine.hpp:562
@@ -689,6 +739,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         // 1 samples the next round into the other buffer.
         const uint64_t B = epoch_B;
         observe_depth(2 * B);
+        AuditLog audit;
         uint64_t max_epochs = (out.omega + B - 1) / B;
         if (opt.max_cycles) max_epochs = std::min(max_epochs, opt.max_cycles);
         max_epochs = std::max<uint64_t>(max_epochs, 1);
@@ -741,7 +792,20 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
             ADSB_CUDA(cudaStreamWaitEvent(s2, samp[k], 0));
             uint32_t* ec = cnt + static_cast<size_t>(k) * n;
             comm_allreduce_u32_sum(opt.comm, ec, n, s2);
+            std::vector<uint32_t> round_counts;
+            if (audit) {
+                round_counts.resize(n);
+                ADSB_CUDA(cudaMemcpyAsync(round_counts.data(), ec, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
+            }
             k_fold_epoch<<<grid_for(n, ctx.device), 256, 0, s2>>>(total, ec, n, dmax + k);
+            if (audit) {
+                uint32_t mx = 0;
+                ADSB_CUDA(cudaMemcpyAsync(&mx, dmax + k, sizeof mx, cudaMemcpyDeviceToHost, s2));
+                ADSB_CUDA(cudaStreamSynchronize(s2));
+                const bool pass = rule_passes_host(mx, (e + 1) * B, rule);
+                audit.words({2, e, B, pass ? 1u : 0u, mx});
+                for (uint32_t x : round_counts) audit.words({x});
+            }
             k_epoch_rule<<<1, 32, 0, s2>>>(dmax + k, (e + 1) * B, rule, flag_dev + k);
             ADSB_CUDA(cudaMemcpyAsync(flag_host + k, flag_dev + k, sizeof(uint32_t), cudaMemcpyDeviceToHost, s2));
             ADSB_CUDA(cudaEventRecord(chk[k], s2));
@@ -784,6 +848,7 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         out.check_cycles = e + 1;
         out.stop_epoch = e + 1;
         out.total_samples = launched * B;
+        if (audit) audit.words({3, out.tau, out.check_cycles});
     }
 
     // ---- results

@@ -61,6 +61,7 @@ struct SamplerParams {
     uint32_t max_degree;    // graph max degree (low-degree graphs use thread-per-vertex expansion)
     uint32_t clear_layout;  // block teams: global state in the cleared layout (else tagged)
     float csr_hint;         // block teams: fraction of CSR reads marked L2 evict_last (1 when the CSR fits L2/2)
+    uint32_t vec4;          // block teams, shared-memory store: 16-byte adjacency vectors (CSR larger than L2)
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode
@@ -101,7 +102,7 @@ struct SamplerParams {
 int sampler_warps_per_sm(bool deterministic);
 void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 // Block-team sampler with shared-memory state (sampler_cta.cu): slots = blocks.
-size_t sampler_cta_smem_bytes(uint32_t hash_cap);
+size_t sampler_cta_smem_bytes(uint32_t hash_cap, bool vec4);
 int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads);
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 int sampler_global_blocks_per_sm();

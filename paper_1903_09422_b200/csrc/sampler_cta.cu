@@ -38,6 +38,9 @@
 #ifndef ADSB_LOAD_BATCH
 #define ADSB_LOAD_BATCH 1  // adjacency loads in flight per thread in for_edges (A/B: 1 beats 2 and 4)
 #endif
+#ifndef ADSB_SMEM_FILTER
+#define ADSB_SMEM_FILTER 0
+#endif
 #ifndef ADSB_GLOBAL_MINB
 #define ADSB_GLOBAL_MINB 4  // min blocks/SM of the global-store-only kernel (256 threads; register budget)
 #endif
@@ -107,14 +110,28 @@ constexpr int kBT = 1024;
 #include "sampler_cta_body.cuh"
 }  // namespace bt1024
 
-size_t sampler_cta_smem_bytes(uint32_t hash_cap) {
-    return static_cast<size_t>(hash_cap) * 12 + static_cast<size_t>(hash_cap / 2) * 4;  // sigma, key|meta, queue
+size_t sampler_cta_smem_bytes(uint32_t hash_cap, bool vec4) {
+    // sigma, key|meta, queue (+ the membership filter) (+ the vector kernels' row ranges)
+    size_t bytes = static_cast<size_t>(hash_cap) * 12 + static_cast<size_t>(hash_cap / 2) * 4;
+#if ADSB_SMEM_FILTER
+    bytes += bt256::SmemStore::kFbWords * 4;
+#endif
+    if (vec4) bytes += 2 * 256 * sizeof(uint32_t);
+    return bytes;
 }
 
 namespace {
 template <class K>
 void allow_big_smem(K kernel) {
-    ADSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    // dynamic shared memory up to 200 KB, within the per-block opt-in limit
+    // left by the kernel's static Shared block
+    int dev = 0, optin = 0;
+    ADSB_CUDA(cudaGetDevice(&dev));
+    ADSB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    ADSB_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    const int room = optin - static_cast<int>(fa.sharedSizeBytes);
+    ADSB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, room)));
 }
 void configure_once() {
     static bool done = false;
@@ -125,6 +142,9 @@ void configure_once() {
     allow_big_smem(bt256::sampler_cta_kernel<kModeDet, false>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, false>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeFused, false>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeDet, false, true>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, false, true>);
+    allow_big_smem(bt256::sampler_cta_kernel<kModeFused, false, true>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeDet, true>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeEpoch, true>);
     allow_big_smem(bt256::sampler_cta_kernel<kModeFused, true>);
@@ -140,7 +160,7 @@ void configure_once() {
 
 int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads) {
     configure_once();
-    const size_t dyn = sampler_cta_smem_bytes(hash_cap);
+    const size_t dyn = sampler_cta_smem_bytes(hash_cap, false);
     int blocks = 0;
     if (block_threads == 128)
         ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<kModeDet, false>, 128, dyn));
@@ -160,7 +180,7 @@ int sampler_global_blocks_per_sm() {
 
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream) {
     configure_once();
-    const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
+    const size_t dyn = sampler_cta_smem_bytes(p.hash_cap, p.vec4 && p.block_threads == 256);
     if (!p.use_smem) {
         const unsigned grid = std::min<unsigned>(p.slots, p.global_grid);
         if (p.global_threads == 1024) {
@@ -177,6 +197,9 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
     if (p.block_threads == 128) {
         if (deterministic) bt128::sampler_cta_kernel<kModeDet, false><<<p.blocks, 128, dyn, stream>>>(p);
         else bt128::sampler_cta_kernel<kModeEpoch, false><<<p.blocks, 128, dyn, stream>>>(p);
+    } else if (p.vec4) {
+        if (deterministic) bt256::sampler_cta_kernel<kModeDet, false, true><<<p.blocks, 256, dyn, stream>>>(p);
+        else bt256::sampler_cta_kernel<kModeEpoch, false, true><<<p.blocks, 256, dyn, stream>>>(p);
     } else {
         if (deterministic) bt256::sampler_cta_kernel<kModeDet, false><<<p.blocks, 256, dyn, stream>>>(p);
         else bt256::sampler_cta_kernel<kModeEpoch, false><<<p.blocks, 256, dyn, stream>>>(p);
@@ -186,7 +209,7 @@ void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t
 
 void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     configure_once();
-    const size_t dyn = sampler_cta_smem_bytes(p.hash_cap);
+    const size_t dyn = sampler_cta_smem_bytes(p.hash_cap, p.vec4 && p.block_threads == 256);
     if (!p.use_smem) {
         if (p.global_threads == 1024)
             bt1024::sampler_cta_kernel<kModeFused, true><<<std::min<unsigned>(p.slots, p.global_grid), 1024, 0, stream>>>(p);
@@ -198,6 +221,7 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
         return;
     }
     if (p.block_threads == 128) bt128::sampler_cta_kernel<kModeFused, false><<<p.blocks, 128, dyn, stream>>>(p);
+    else if (p.vec4) bt256::sampler_cta_kernel<kModeFused, false, true><<<p.blocks, 256, dyn, stream>>>(p);
     else bt256::sampler_cta_kernel<kModeFused, false><<<p.blocks, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
 }

@@ -63,8 +63,14 @@ struct Shared {
 // Shared-memory open-addressing table: km = key << 32 | meta, sig = sigma.
 // Empty slots have key 0xFFFFFFFF and sigma 0 (sigma is zeroed with the key,
 // so concurrent claimers and adders never race on initialisation).
-struct SmemStore {
+template <bool kVec>
+struct SmemStoreT {
     static constexpr uint32_t kLoadBatch = ADSB_LOAD_BATCH;
+    static constexpr bool kVec4 = kVec;  // flattened adjacency read as 16-byte vectors
+    // vectorised reads: each chunk vertex's adjacency range [off(u), off(u+1))
+    // as lo[kBT] then hi[kBT], in dynamic shared memory (vector kernels only:
+    // a larger static block would shrink the L1 the scalar kernels prefetch into)
+    uint32_t* crange;
     // Entry = one u32: (vertex + 1) << 8 | meta8 (bit 7 t-side, bit 6 DAG,
     // bits 0-5 distance); 0 = empty. Needs n < 2^24 - 1 and distances <= 63
     // (larger graphs use the global store; a deeper level overflows to it).
@@ -82,6 +88,14 @@ struct SmemStore {
     Shared* sh;
     uint32_t* ins_ctr;  // this level's reservation counter (Shared::lvl_ins slot)
     uint32_t ins_base;  // reservations made before this level (same in every thread)
+#if ADSB_SMEM_FILTER
+    // Membership filter of the claimed vertices (kFbBits bits, one hash): a
+    // probe whose bit is clear skips the table walk. The meeting level's
+    // probes, the bulk of a sample's adjacency, almost all miss.
+    uint32_t* fb;
+    static constexpr uint32_t kFbLog = 15, kFbWords = (1u << kFbLog) / 32;
+    static __device__ __forceinline__ uint32_t fbh(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - kFbLog); }
+#endif
 
     static __device__ __forceinline__ uint32_t decode(uint32_t w) {
         return ((w & 0x80u) ? kMetaT : 0u) | ((w & 0x40u) ? kMetaDag : 0u) | (w & 0x3Fu);
@@ -101,6 +115,9 @@ struct SmemStore {
             km[i] = 0u;
             sig[i] = 0ull;
         }
+#if ADSB_SMEM_FILTER
+        for (uint32_t i = tid; i < kFbWords; i += kBT) fb[i] = 0u;
+#endif
     }
     __device__ void begin(uint32_t tid) {
 #ifdef ADSB_DEBUG_CHECKS
@@ -131,10 +148,19 @@ struct SmemStore {
                 const uint32_t h = qv[i < ns ? i : tpos(i - ns)];
                 if (h != kNone) km[h] = 0u;
             }
+#if ADSB_SMEM_FILTER
+            for (uint32_t i = C.tid; i < kFbWords; i += kBT) fb[i] = 0u;
+#endif
         }
         __syncthreads();
     }
     __device__ uint32_t find(uint32_t v, uint32_t& meta) const {
+#if ADSB_SMEM_FILTER
+        {
+            const uint32_t f = fbh(v);
+            if (!(fb[f >> 5] & (1u << (f & 31)))) return kNone;
+        }
+#endif
         const uint32_t key = v + 1u;
         uint32_t h = home(v);
         for (;;) {
@@ -175,6 +201,10 @@ struct SmemStore {
                 if (prev == 0u) {
                     inserted = true;
                     meta = new_meta;
+#if ADSB_SMEM_FILTER
+                    const uint32_t f = fbh(v);
+                    atomicOr(fb + (f >> 5), 1u << (f & 31));
+#endif
                     return h;
                 }
                 if ((prev >> 8) == key) {
@@ -223,6 +253,7 @@ struct SmemStore {
         return ins_base < limit && edges <= limit - ins_base;
     }
 };
+using SmemStore = SmemStoreT<false>;
 
 // Per-team dense global state, 2 words per vertex, in one of two layouts
 // chosen per graph (SamplerParams::clear_layout; the engine zeroes the arena
@@ -270,6 +301,7 @@ struct SmemStore {
 template <uint32_t kU, bool kBatch = false>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
+    static constexpr bool kVec4 = false;
     static constexpr bool kBatchClaims = kBatch;  // global-store-only kernels
     static constexpr bool kSlotIsVertex = true;   // find() returns the vertex as its slot
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
@@ -398,19 +430,44 @@ struct GlobalStoreT {
 // CSR reads carry an L2 eviction-priority hint: evict_last when the CSR fits
 // in a fraction of L2 (SamplerParams::csr_hint = 1), so the per-sample state
 // streaming through L2 (C4: ~10 GB per 1k samples) does not evict it.
-__device__ __forceinline__ uint32_t ld_csr(const uint32_t* p, float frac) {
+#ifndef ADSB_POL_HOIST
+#define ADSB_POL_HOIST 1  // the L2 policy is created once per kernel, not per CSR load
+#endif
+__device__ __forceinline__ unsigned long long csr_policy(float frac) {
     unsigned long long pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(frac));
+    return pol;
+}
+__device__ __forceinline__ uint32_t ld_csr_pol(const uint32_t* p, unsigned long long pol) {
     uint32_t v;
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_csr(const uint32_t* p, float frac) { return ld_csr_pol(p, csr_policy(frac)); }
+__device__ __forceinline__ uint4 ld_csr4_pol(const uint4* p, unsigned long long pol) {
+    uint4 v;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p), "l"(pol));
     return v;
 }
 struct Ctx {
     const uint32_t* __restrict__ off;
     const uint32_t* __restrict__ nbrs;
     float csr_hint;
+#if ADSB_POL_HOIST
+    unsigned long long pol;
+    __device__ __forceinline__ uint32_t O(size_t i) const { return ld_csr_pol(off + i, pol); }
+    __device__ __forceinline__ uint32_t N(size_t i) const { return ld_csr_pol(nbrs + i, pol); }
+    // the 16-byte vector holding adjacency entries 4g .. 4g+3 (cudaMalloc aligns nbrs)
+    __device__ __forceinline__ uint4 N4(size_t g) const { return ld_csr4_pol(reinterpret_cast<const uint4*>(nbrs) + g, pol); }
+#else
     __device__ __forceinline__ uint32_t O(size_t i) const { return ld_csr(off + i, csr_hint); }
     __device__ __forceinline__ uint32_t N(size_t i) const { return ld_csr(nbrs + i, csr_hint); }
+    __device__ __forceinline__ uint4 N4(size_t g) const {
+        return ld_csr4_pol(reinterpret_cast<const uint4*>(nbrs) + g, csr_policy(csr_hint));
+    }
+#endif
     uint32_t tid;
     uint32_t lane;
     uint32_t warp;
@@ -449,6 +506,9 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 // of one dependent round trip per neighbour.
 #ifndef ADSB_LOWDEG_BATCH
 #define ADSB_LOWDEG_BATCH 1
+#endif
+#ifndef ADSB_LEAN_LOOP
+#define ADSB_LEAN_LOOP 0
 #endif
 constexpr unsigned long long kNoTok = ~0ull;
 template <class Store, class Prep, class Issue, class Body>
@@ -528,6 +588,85 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         __syncthreads();
         return;
     }
+    if constexpr (Store::kVec4) {
+    // Vectorised flattening: each frontier vertex's adjacency [o, e) is covered
+    // by the 16-byte vectors floor(o/4) .. ceil(e/4)-1; the block scans vector
+    // counts and thread t takes vectors t, t+kBT, ... of the chunk, so one load
+    // brings 4 ids (a hub row: 4 real edges per load; entries of the vector
+    // outside [o, e) are skipped). 4x the bytes in flight per load instruction.
+    for (uint32_t base = lo; base < hi; base += kBT) {
+        ADSB_PHASE_MARK(f0);
+        const uint32_t i = base + C.tid;
+        uint32_t nv = 0, o = 0, e = 0, slot = 0;
+        unsigned long long val = 0;
+        if (i < hi) {
+            const uint32_t q = t_list ? S.tpos(i) : i;
+            const uint32_t u = S.qv[q];
+            ADSB_DCHECK(u < C.n);
+            o = C.O(u);
+            e = C.O(u + 1);
+            nv = e > o ? ((e + 3) >> 2) - (o >> 2) : 0u;
+            uint32_t meta;
+            slot = S.find(u, meta);
+            val = prep(slot, meta, e - o);
+        }
+        const uint32_t wdeg = __reduce_add_sync(kFull, e - o);
+        if (C.lane == 0 && wdeg) counter[C.warp] += wdeg;
+        uint32_t total;
+        const uint32_t incl = block_inclusive_sum(C, nv, total);
+        sh.scan[C.tid] = incl;
+        sh.cbase[C.tid] = (o >> 2) - (incl - nv);
+        S.crange[C.tid] = o;
+        S.crange[kBT + C.tid] = e;
+        sh.cslot[C.tid] = slot;
+        sh.cval[C.tid] = val;
+        __syncthreads();
+        ADSB_PHASE_MARK(f1);
+        ADSB_PHASE_ADD(8, f1 - f0);
+        ADSB_PHASE_ADD(12, total);
+        ADSB_PHASE_ADD(13, 1);
+        const uint32_t populated = min(hi - base, static_cast<uint32_t>(kBT));
+        uint32_t ow = 0, o_end = 0, o_base = 0, r_lo = 0, r_hi = 0, o_slot = 0;
+        unsigned long long o_val = 0;
+        bool have = false;
+        for (uint32_t j = C.tid; j < total; j += kBT) {
+            if (!have || j >= o_end) {
+                uint32_t l = have ? ow + 1 : 0, r = populated - 1;
+                while (l < r) {
+                    const uint32_t mid = (l + r) >> 1;
+                    if (sh.scan[mid] > j) r = mid;
+                    else l = mid + 1;
+                }
+                ow = l;
+                o_end = sh.scan[ow];
+                o_base = sh.cbase[ow];
+                r_lo = S.crange[ow];
+                r_hi = S.crange[kBT + ow];
+                o_slot = sh.cslot[ow];
+                o_val = sh.cval[ow];
+                have = true;
+            }
+            const uint32_t g = o_base + j;
+            const uint4 x = C.N4(g);
+            if (j + ADSB_PF_DIST * kBT < o_end)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const uint4*>(C.nbrs) + g + ADSB_PF_DIST * kBT));
+            const uint32_t e0 = g * 4u;
+#pragma unroll 1
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t idx = e0 + k;
+                if (idx < r_lo || idx >= r_hi) continue;
+                const uint32_t v = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
+                ADSB_DCHECK(v < C.n);
+                body(o_slot, o_val, v, kNoTok);
+            }
+        }
+        ADSB_PHASE_MARK(f2);
+        __syncthreads();
+        ADSB_PHASE_MARK(f3);
+        ADSB_PHASE_ADD(9, f2 - f1);
+        ADSB_PHASE_ADD(11, f3 - f2);
+    }
+    } else {
     for (uint32_t base = lo; base < hi; base += kBT) {
         ADSB_PHASE_MARK(f0);
         const uint32_t i = base + C.tid;
@@ -572,6 +711,36 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         constexpr uint32_t kBatch = Store::kLoadBatch;
         constexpr uint32_t kOwnerBits = kBT <= 256 ? 8 : 16;
         static_assert(kBT <= 65536 && kBatch * kOwnerBits <= 32, "owner indices pack into 32 bits");
+#if ADSB_LEAN_LOOP
+        if constexpr (kBatch == 1) {
+            // One load per iteration: the owner's row (end, base, slot, payload)
+            // stays in registers until the edge index leaves it, so a hub row
+            // costs no shared-memory reads per edge.
+            uint32_t o_slot = 0;
+            unsigned long long o_val = 0;
+            for (uint32_t e = C.tid; e < total; e += kBT) {
+                if (!have || e >= o_end) {
+                    uint32_t l = have ? ow + 1 : 0, r = populated - 1;
+                    while (l < r) {
+                        const uint32_t mid = (l + r) >> 1;
+                        if (sh.scan[mid] > e) r = mid;
+                        else l = mid + 1;
+                    }
+                    ow = l;
+                    o_end = sh.scan[ow];
+                    o_base = sh.cbase[ow];
+                    o_slot = sh.cslot[ow];
+                    o_val = sh.cval[ow];
+                    have = true;
+                }
+                const uint32_t v = C.N(o_base + e);
+                if (e + ADSB_PF_DIST * kBT < o_end)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(C.nbrs + o_base + e + ADSB_PF_DIST * kBT));
+                ADSB_DCHECK(v < C.n);
+                body(o_slot, o_val, v, kNoTok);
+            }
+        } else
+#endif
         for (uint32_t e0 = C.tid; e0 < total; e0 += kBT * kBatch) {
             uint32_t owners = 0, cnt = 0;
             uint32_t vv[kBatch];
@@ -616,6 +785,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         ADSB_PHASE_MARK(f3);
         ADSB_PHASE_ADD(9, f2 - f1);
         ADSB_PHASE_ADD(11, f3 - f2);
+    }
     }
 }
 
@@ -1427,13 +1597,20 @@ extern __shared__ unsigned long long adsb_dyn[];
 
 // Store descriptors are rebuilt per sample from the launch parameters rather
 // than kept live across the sample loop (register budget: 64 per thread).
-__device__ __forceinline__ SmemStore make_smem_store(const SamplerParams& p, Shared& sh) {
-    SmemStore sm;
+template <bool kVec = false>
+__device__ __forceinline__ SmemStoreT<kVec> make_smem_store(const SamplerParams& p, Shared& sh) {
+    SmemStoreT<kVec> sm;
     const uint32_t H = p.hash_cap;
     sm.sig = adsb_dyn;                                     // H x u64
     sm.km = reinterpret_cast<uint32_t*>(adsb_dyn + H);     // H x u32
     sm.qcap = H / 2;
     sm.qv = sm.km + H;                                     // H/2 x u32
+    uint32_t* tail = sm.qv + H / 2;
+#if ADSB_SMEM_FILTER
+    sm.fb = tail;                                          // kFbWords x u32
+    tail += SmemStoreT<kVec>::kFbWords;
+#endif
+    sm.crange = kVec ? tail : nullptr;                     // 2 kBT x u32 (vector kernels)
     sm.tlev = sh.tlev_small;
     sm.slev = sh.slev_small;
     sm.cap = H;
@@ -1493,7 +1670,7 @@ __device__ void release_region(const SamplerParams& p, uint32_t region, uint32_t
 }
 
 // gtag: the global-only kernel's generation tag for its own region (block-uniform).
-template <int kMode, bool kGlobalOnly>
+template <int kMode, bool kGlobalOnly, bool kVec>
 __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint32_t frame_local, uint32_t& gtag) {
     const uint32_t s = static_cast<uint32_t>(rng.next_below(p.n));
     uint32_t t = static_cast<uint32_t>(rng.next_below(p.n - 1));
@@ -1504,7 +1681,7 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
     int rc = 1;
     if constexpr (!kGlobalOnly) {
         if (p.use_smem) {
-            SmemStore sm = make_smem_store(p, *C.sh);
+            auto sm = make_smem_store<kVec>(p, *C.sh);
             rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
         }
     }
@@ -1658,7 +1835,10 @@ __device__ void fold_chain(Ctx& C, const SamplerParams& p) {
     }
 }
 
-template <int kMode, bool kGlobalOnly>
+// kVec: the shared-memory store's flattened adjacency reads are 16-byte
+// vectors (chosen for graphs whose CSR misses L2, where bytes in flight per
+// load matter; scalar reads win on L2-resident CSRs).
+template <int kMode, bool kGlobalOnly, bool kVec = false>
 __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kBT : ADSB_MINB_PER_256 * 256 / kBT)
     sampler_cta_kernel(SamplerParams p) {
     __shared__ Shared sh;
@@ -1666,6 +1846,9 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
     C.off = p.off;
     C.nbrs = p.nbrs;
     C.csr_hint = p.csr_hint;
+#if ADSB_POL_HOIST
+    C.pol = csr_policy(p.csr_hint);
+#endif
     C.tid = threadIdx.x;
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
@@ -1704,7 +1887,7 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
             SplitMix64 rng(reseed(p.seed, p.first + local));
             for (uint64_t i = 0; i < p.spf; ++i) {
                 if (C.tid == 0) sh.n_samples += 1;
-                one_sample<kMode, kGlobalOnly>(C, p, rng, static_cast<uint32_t>(local), gtag);
+                one_sample<kMode, kGlobalOnly, kVec>(C, p, rng, static_cast<uint32_t>(local), gtag);
             }
         }
     } else {
@@ -1765,7 +1948,7 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
             SplitMix64 rng(reseed(p.seed, item));
             if (C.tid == 0) sh.n_samples += 1;
             const uint32_t rec0 = sh.recorded;
-            one_sample<kMode, kGlobalOnly>(C, p, rng, k, gtag);
+            one_sample<kMode, kGlobalOnly, kVec>(C, p, rng, k, gtag);
             if (C.tid == 0) {
                 if (p.audit && item < p.max_epochs * p.epoch_b)
                     p.audit[item] = (sh.recorded - rec0) | (sh.last_d << 16);

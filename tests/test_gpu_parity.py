@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1903_09422_b200 import adsamp, datasets
+from paper_1903_09422_b200 import adsamp, datasets, kadabra
 from paper_1903_09422_b200.adsamp import EngineConfig, Variant
 from paper_1903_09422_b200.kadabra import estimate_bc, sample_frames
 
@@ -158,13 +158,15 @@ def test_single_vertex_and_errors():
         estimate_bc(g, 0.1, 0.0, EngineConfig())
 
 
-@pytest.mark.parametrize("mode", ["block", "block-global", "block-tinyhash", "warp"])
+@pytest.mark.parametrize("mode", ["block", "block-vec4", "block-global", "block-tinyhash", "warp"])
 def test_sampler_variants_bit_exact(mode, monkeypatch, grid200):
     """All sampler implementations (block teams with the shared-memory table,
-    block teams forced onto global state, a table so small that most samples
-    overflow and are redone, warp teams) give the same paths and results."""
+    with scalar or 16-byte vector adjacency reads, block teams forced onto
+    global state, a table so small that most samples overflow and are redone,
+    warp teams) give the same paths and results."""
     monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
     monkeypatch.delenv("ADSB_HASH_CAP", raising=False)
+    monkeypatch.setenv("ADSB_VEC4", "1" if mode == "block-vec4" else "0")
     monkeypatch.setenv("ADSB_SAMPLER", "warp" if mode == "warp" else "block")  # small n would pick warps
     if mode == "block-global":
         monkeypatch.setenv("ADSB_NO_SMEM", "1")
@@ -262,7 +264,7 @@ def test_epoch_block_teams_fused_and_host_driven(fused, B, monkeypatch):
     assert r.tau == 3 * B and r.reason.name == "capped"
 
 
-@pytest.mark.parametrize("mode", ["block", "block-global", "block-128"])
+@pytest.mark.parametrize("mode", ["block", "block-vec4", "block-global", "block-128"])
 @pytest.mark.parametrize("spf", [1, 4])
 def test_block_teams_frames_ba(mode, spf, monkeypatch):
     """Block teams on a hub-heavy BA graph (shared-memory table overflows for
@@ -271,6 +273,7 @@ def test_block_teams_frames_ba(mode, spf, monkeypatch):
     monkeypatch.setenv("ADSB_SAMPLER", "block")
     monkeypatch.delenv("ADSB_NO_SMEM", raising=False)
     monkeypatch.delenv("ADSB_BLOCK", raising=False)
+    monkeypatch.setenv("ADSB_VEC4", "1" if mode == "block-vec4" else "0")
     if mode == "block-global":
         monkeypatch.setenv("ADSB_NO_SMEM", "1")
     elif mode == "block-128":
@@ -315,3 +318,128 @@ def test_fused_epoch_audit_replay(tmp_path, monkeypatch):
     np.testing.assert_array_equal(folded[:stop], rec.reshape(stop, B).sum(axis=1))
     assert not folded[stop:].any()
     assert int(folded[:stop].sum()) == int(r.run.data.sum())
+
+
+def _read_audit(path):
+    w = np.fromfile(path, dtype=np.uint64)
+    i, recs = 0, []
+    while i < w.size:
+        kind = int(w[i])
+        if kind == 1:
+            first, F, cnt, limit, stopped, bm = (int(x) for x in w[i + 1:i + 7])
+            i += 7
+            run_max = w[i:i + F].astype(np.int64)
+            i += F
+            ev = w[i:i + cnt]
+            i += cnt
+            recs.append(("batch", first, F, limit, stopped, bm, run_max, ev))
+        elif kind == 2:
+            e, B, ok, mx = (int(x) for x in w[i + 1:i + 5])
+            i += 5
+            recs.append(("round", e, B, ok, mx, w[i:i + recs_n[0]].astype(np.int64)))
+            i += recs_n[0]
+        elif kind == 3:
+            recs.append(("end", int(w[i + 1]), int(w[i + 2])))
+            i += 3
+        else:
+            raise AssertionError(f"bad audit record {kind}")
+    return recs
+
+
+recs_n = [0]
+
+
+@pytest.mark.parametrize("variant,extra", [(Variant.indexed, {"samples_per_frame": 1}),
+                                           (Variant.indexed, {"samples_per_frame": 3}),
+                                           (Variant.shared, {"epoch_samples": 256})])
+def test_frames_pipeline_audit_replay(tmp_path, monkeypatch, variant, extra):
+    """validate_consistency replay (audit.hpp:101-161 analogue) of the frame
+    pipeline — the deterministic batches and the multi-rank epoch path (epochs
+    as single-sample frames checked every B): every frame's increments equal
+    the oracle's path(s) for that stream position, every check record (the
+    running max after each frame) equals the max count replayed from the event
+    log, the stop frame is the first whose check passes, and the final counts
+    are exactly the events of the frames up to it."""
+    audit = tmp_path / "audit.bin"
+    monkeypatch.setenv("ADSB_AUDIT", str(audit))
+    monkeypatch.setenv("ADSB_SAMPLER", "warp")
+    pairs = datasets.pairs("c1_er")
+    pg, og = both(pairs)
+    n = pg.graph.num_vertices()
+    eps = 0.03
+    cfg = EngineConfig(variant=variant, threads=8, base_seed=9, device=0, **extra)
+    r = estimate_bc(pg.graph, eps, 0.1, cfg)
+    recs_n[0] = n
+    recs = _read_audit(audit)
+    spf = extra.get("samples_per_frame", 1)
+    C = extra.get("epoch_samples", 1)
+    counts = np.zeros(n, np.int64)
+    run_max_all = 0
+    stop_frame = None
+    for rec in recs:
+        if rec[0] != "batch":
+            continue
+        _, first, F, limit, stopped, bm, run_max, ev = rec
+        assert bm == run_max_all
+        ev = ev[ev != np.uint64(0xFFFFFFFFFFFFFFFF)]
+        v = (ev >> np.uint64(32)).astype(np.int64)
+        f = (ev & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        paths = oracle.sample_frames(og, 9, spf, first, F)
+        order = np.argsort(f, kind="stable")
+        v, f = v[order], f[order]
+        bounds = np.searchsorted(f, np.arange(F + 1))
+        cur = counts.copy()
+        mx = 0
+        for k in range(F):
+            got = np.sort(v[bounds[k]:bounds[k + 1]])
+            np.testing.assert_array_equal(got, np.sort(paths[k].astype(np.int64)))
+            for x in got:
+                cur[x] += 1
+                mx = max(mx, int(cur[x]))
+            assert int(run_max[k]) == mx, (first, k)
+        # frames <= limit are folded
+        for k in range(limit + 1):
+            np.add.at(counts, v[bounds[k]:bounds[k + 1]], 1)
+        run_max_all = max(run_max_all, int(run_max[limit]))
+        if stopped:
+            stop_frame = first + limit
+    assert stop_frame is not None
+    tau = (stop_frame + 1) * spf
+    assert r.tau == tau and recs[-1] == ("end", tau, (stop_frame + 1) // C)
+    np.testing.assert_array_equal(r.run.data.astype(np.int64), counts)
+    # the stop check holds with the reference's all-vertex rule (kadabra_check)
+    assert kadabra.kadabra_check(counts, tau, r.omega, eps, 0.1)
+
+
+def test_barrier_rounds_audit_replay(tmp_path, monkeypatch):
+    """The barrier variant's round pipeline (dense all-reduce of the n-length
+    round counts, used across GPUs): every round's counts equal the oracle's
+    paths for that round's sample indices, every check's max and verdict are
+    reproduced from the running total, and the result is the total at the
+    first passing round."""
+    audit = tmp_path / "audit.bin"
+    monkeypatch.setenv("ADSB_AUDIT", str(audit))
+    monkeypatch.setenv("ADSB_DENSE_EPOCHS", "1")
+    monkeypatch.setenv("ADSB_NO_FUSED", "1")
+    pairs = datasets.pairs("c1_er")
+    pg, og = both(pairs)
+    n = pg.graph.num_vertices()
+    eps, B = 0.03, 500
+    cfg = EngineConfig(variant=Variant.barrier, threads=8, base_seed=4, check_interval=B, device=0)
+    r = estimate_bc(pg.graph, eps, 0.1, cfg)
+    recs_n[0] = n
+    recs = [x for x in _read_audit(audit) if x[0] == "round"]
+    total = np.zeros(n, np.int64)
+    for _, e, B_, ok, mx, cnt in recs:
+        assert B_ == B
+        want = np.zeros(n, np.int64)
+        for p in oracle.sample_frames(og, 4, 1, e * B, B):
+            np.add.at(want, p.astype(np.int64), 1)
+        np.testing.assert_array_equal(cnt, want)
+        total += cnt
+        assert mx == int(total.max())
+        assert bool(ok) == kadabra.kadabra_check(total, (e + 1) * B, r.omega, eps, 0.1)
+        if ok:
+            break
+    assert r.tau == (recs[-1][1] + 1) * B
+    np.testing.assert_array_equal(r.run.data.astype(np.int64), total)
