@@ -4,6 +4,10 @@
 
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kMaxHubs = 32;
+#ifndef ADSB_HUB_PROBE
+#define ADSB_HUB_PROBE 1
+#endif
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kMetaT = 1u << 31;
@@ -54,6 +58,11 @@ struct Shared {
     unsigned long long ev_pos;
     unsigned long long fold_epoch;    // fused mode: epoch being folded
     uint32_t fold_len, fold_max, flag;
+    // probe passes: frontier hubs searched against the other side's level list
+    // instead of scanned (for_edges_tok, kMaxHubs per chunk)
+    uint32_t n_hub[2];
+    uint32_t hub_o[kMaxHubs], hub_e[kMaxHubs], hub_slot[kMaxHubs];
+    unsigned long long hub_val[kMaxHubs];
 };
 
 // ---------------------------------------------------------------------------
@@ -511,9 +520,46 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 #define ADSB_LEAN_LOOP 0
 #endif
 constexpr unsigned long long kNoTok = ~0ull;
+// Probe passes may pass the other side's last level [l_lo, l_hi) (t-side
+// queue entries when l_t): a frontier vertex whose adjacency is much longer
+// than that list (deg > 4 |L| log2 deg) is not scanned; instead every list
+// vertex is binary-searched in its ascending adjacency (the same edges, found
+// in |L| log deg reads: C5's meeting probes are dominated by a few hubs
+// against ~1k-vertex levels). body runs once per found edge, as for scanned ones.
+__device__ __forceinline__ bool hub_search(const Ctx& C, uint32_t o, uint32_t e, uint32_t v) {
+    uint32_t l = o, r = e;
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        if (C.N(mid) < v) l = mid + 1;
+        else r = mid;
+    }
+    return l < e && C.N(l) == v;
+}
+__device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list) {
+    return ADSB_HUB_PROBE && list && deg > 4u * list * (32u - __clz(deg));
+}
+// The chunk's hubs against the level list: pair (h, j) per thread, one binary
+// search each. The hub list is complete (filled before the chunk's scan barrier).
+template <class Store, class Body>
+__device__ __forceinline__ void hub_phase(Ctx& C, Store& S, Shared& sh, uint32_t par, uint32_t l_lo, uint32_t l_hi,
+                                          bool l_t, Body& body) {
+    if (l_hi <= l_lo) return;
+    const uint32_t nh = min(sh.n_hub[par], kMaxHubs);
+    if (nh == 0) return;
+    const uint32_t L = l_hi - l_lo;
+    const uint32_t pairs = nh * L;
+    for (uint32_t pi = C.tid; pi < pairs; pi += kBT) {
+        const uint32_t h = pi / L, j = pi - h * L;
+        const uint32_t q = l_lo + j;
+        const uint32_t v = S.qv[l_t ? S.tpos(q) : q];
+        if (hub_search(C, sh.hub_o[h], sh.hub_e[h], v)) body(sh.hub_slot[h], sh.hub_val[h], v, kNoTok);
+    }
+}
+
 template <class Store, class Prep, class Issue, class Body>
 __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long* counter,
-                              Prep prep, Issue issue, Body body) {
+                              Prep prep, Issue issue, Body body, uint32_t l_lo = 0, uint32_t l_hi = 0,
+                              bool l_t = false) {
     Shared& sh = *C.sh;
     ADSB_PHASE_ADD(6, 1);
     if (C.low_degree) {
@@ -599,6 +645,9 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         const uint32_t i = base + C.tid;
         uint32_t nv = 0, o = 0, e = 0, slot = 0;
         unsigned long long val = 0;
+        const uint32_t par = ((base - lo) / kBT) & 1u;
+        if (C.tid == 0) sh.n_hub[par ^ 1u] = 0;
+        uint32_t scanned = 0;
         if (i < hi) {
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
@@ -609,8 +658,20 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             uint32_t meta;
             slot = S.find(u, meta);
             val = prep(slot, meta, e - o);
+            scanned = e - o;
+            if (is_hub(e - o, l_hi - l_lo)) {
+                const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
+                if (h < kMaxHubs) {
+                    sh.hub_o[h] = o;
+                    sh.hub_e[h] = e;
+                    sh.hub_slot[h] = slot;
+                    sh.hub_val[h] = val;
+                    nv = 0;
+                    scanned = (l_hi - l_lo) * (32u - __clz(e - o));  // searches, not scans
+                }
+            }
         }
-        const uint32_t wdeg = __reduce_add_sync(kFull, e - o);
+        const uint32_t wdeg = __reduce_add_sync(kFull, scanned);
         if (C.lane == 0 && wdeg) counter[C.warp] += wdeg;
         uint32_t total;
         const uint32_t incl = block_inclusive_sum(C, nv, total);
@@ -660,6 +721,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                 body(o_slot, o_val, v, kNoTok);
             }
         }
+        hub_phase(C, S, sh, par, l_lo, l_hi, l_t, body);
         ADSB_PHASE_MARK(f2);
         __syncthreads();
         ADSB_PHASE_MARK(f3);
@@ -672,6 +734,9 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         const uint32_t i = base + C.tid;
         uint32_t deg = 0, o = 0, slot = 0;
         unsigned long long val = 0;
+        const uint32_t par = ((base - lo) / kBT) & 1u;
+        if (C.tid == 0) sh.n_hub[par ^ 1u] = 0;
+        uint32_t hub_reads = 0;
         if (i < hi) {
             const uint32_t q = t_list ? S.tpos(i) : i;
             const uint32_t u = S.qv[q];
@@ -681,6 +746,21 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             uint32_t meta;
             slot = S.find(u, meta);
             val = prep(slot, meta, deg);
+            if (is_hub(deg, l_hi - l_lo)) {
+                const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
+                if (h < kMaxHubs) {
+                    sh.hub_o[h] = o;
+                    sh.hub_e[h] = o + deg;
+                    sh.hub_slot[h] = slot;
+                    sh.hub_val[h] = val;
+                    hub_reads = (l_hi - l_lo) * (32u - __clz(deg));
+                    deg = 0;
+                }
+            }
+        }
+        {
+            const uint32_t wr = __reduce_add_sync(kFull, hub_reads);
+            if (C.lane == 0 && wr) counter[C.warp] += wr;
         }
         uint32_t total;
         const uint32_t incl = block_inclusive_sum(C, deg, total);
@@ -780,6 +860,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                 for (uint32_t j = 0; j + 1 < kBatch; ++j) vv[j] = vv[j + 1];
             }
         }
+        hub_phase(C, S, sh, par, l_lo, l_hi, l_t, body);
         ADSB_PHASE_MARK(f2);
         __syncthreads();
         ADSB_PHASE_MARK(f3);
@@ -791,9 +872,11 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
 
 template <class Store, class Prep, class Body>
 __device__ __forceinline__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list,
-                                          unsigned long long* counter, Prep prep, Body body) {
+                                          unsigned long long* counter, Prep prep, Body body, uint32_t l_lo = 0,
+                                          uint32_t l_hi = 0, bool l_t = false) {
     for_edges_tok(C, S, lo, hi, t_list, counter, prep, [](uint32_t) { return kNoTok; },
-                  [&](uint32_t su, unsigned long long val, uint32_t v, unsigned long long) { body(su, val, v); });
+                  [&](uint32_t su, unsigned long long val, uint32_t v, unsigned long long) { body(su, val, v); },
+                  l_lo, l_hi, l_t);
 }
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int src) {
@@ -982,7 +1065,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (t_lo == t_hi) return {a, b, 2};
             deg_t = by_count ? t_hi - t_lo : level_degrees(C, S, t_lo, t_hi, true, cur);
         } else if (deg_s <= deg_t) {
-            // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b)
+            // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b);
+            // hubs of the frontier are searched for T_b's vertices instead of scanned
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
             for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
@@ -994,7 +1078,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               if (!(m & kMetaDag)) S.set_dag(sl);
                               sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           }
-                      });
+                      },
+                      t_lo, t_hi, true);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
@@ -1033,7 +1118,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             if (s_lo == s_hi) return {a, b, 2};
             deg_s = by_count ? s_hi - s_lo : level_degrees(C, S, s_lo, s_hi, false, cur);
         } else {
-            // ---- t-side level b: probe for the s-ball
+            // ---- t-side level b: probe for the s-ball (hubs searched for S_a's vertices)
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -1045,7 +1130,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                               S.set_dag(su_slot);
                               sh.lvl_met[cur] = 1u;  // read after for_edges' closing barrier
                           }
-                      });
+                      },
+                      s_lo, s_hi, false);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
