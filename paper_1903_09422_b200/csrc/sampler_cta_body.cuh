@@ -634,6 +634,10 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
         __syncthreads();
         return;
     }
+    if (l_hi > l_lo) {  // probe pass with a level list: hub counters start at 0
+        if (C.tid == 0) sh.n_hub[0] = sh.n_hub[1] = 0;
+        __syncthreads();
+    }
     if constexpr (Store::kVec4) {
     // Vectorised flattening: each frontier vertex's adjacency [o, e) is covered
     // by the 16-byte vectors floor(o/4) .. ceil(e/4)-1; the block scans vector

@@ -1,0 +1,27 @@
+# Round 2 profiles: bench lines (C5 default + C1..C4), launch list of the default bench, ncu --set full (+ L2 bytes)
+# of the sampler kernel on every config. Each ncu command follows the same plain command (exit 0) with &&.
+mkdir -p gpurun_out/r2p; rm -f gpurun_out/r2p/*
+export ADSB_GRAPH_CACHE=build/gcache
+M="--metrics lts__t_bytes.sum,lts__t_sectors.sum,lts__t_sector_hit_rate.pct"
+timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/r2p/bench_c5.log 2>&1
+for c in c1_er c2_rmat18 c3_ba; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/r2p/bench_$c.log 2>&1; done
+timeout 900 python bench.py --config c4_grid --steps 2 --warmup 3 > gpurun_out/r2p/bench_c4_grid.log 2>&1
+timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2p/plain_launches.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+  --log-file gpurun_out/r2p/launches_c5.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2p/ncu_launches.log 2>&1
+timeout 600 python scripts/prof_capped.py c5_rmat24 64 > gpurun_out/r2p/plain_c5.log 2>&1 && \
+timeout 1500 ncu --set full $M --clock-control none --import-source on -k regex:sampler_cta_kernel -c 1 \
+  -o gpurun_out/r2p/c5_full python scripts/prof_capped.py c5_rmat24 64 > gpurun_out/r2p/ncu_c5.log 2>&1
+timeout 300 python scripts/prof_one.py c2_rmat18 2 > gpurun_out/r2p/plain_c2.log 2>&1 && \
+timeout 900 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -s 1 -c 1 \
+  -o gpurun_out/r2p/c2_full python scripts/prof_one.py c2_rmat18 2 > gpurun_out/r2p/ncu_c2.log 2>&1
+timeout 300 python scripts/prof_one.py c3_ba 1 > gpurun_out/r2p/plain_c3.log 2>&1 && \
+timeout 900 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -s 2 -c 1 \
+  -o gpurun_out/r2p/c3_full python scripts/prof_one.py c3_ba 1 > gpurun_out/r2p/ncu_c3.log 2>&1
+timeout 300 python scripts/prof_one.py c1_er 1 > gpurun_out/r2p/plain_c1.log 2>&1 && \
+timeout 900 ncu --set full $M --clock-control none -k regex:sampler_kernel -c 1 \
+  -o gpurun_out/r2p/c1_full python scripts/prof_one.py c1_er 1 > gpurun_out/r2p/ncu_c1.log 2>&1
+timeout 600 python scripts/prof_capped.py c4_grid 1184 > gpurun_out/r2p/plain_c4.log 2>&1 && \
+timeout 1500 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -c 1 \
+  -o gpurun_out/r2p/c4_full python scripts/prof_capped.py c4_grid 1184 > gpurun_out/r2p/ncu_c4.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2p/smoke.log 2>&1
