@@ -62,6 +62,7 @@ struct SamplerParams {
     uint32_t clear_layout;  // block teams: global state in the cleared layout (else tagged)
     float csr_hint;         // block teams: fraction of CSR reads marked L2 evict_last (1 when the CSR fits L2/2)
     uint32_t vec4;          // block teams, shared-memory store: 16-byte adjacency vectors (CSR larger than L2)
+    uint32_t hub_factor;    // probe passes: search a frontier row of degree > (hub_factor/4) |L| log2(deg) (0 = never)
     // work: items [0, num_items) map to stream positions first + item*world + rank
     uint64_t seed;
     uint64_t spf;          // samples per item (deterministic frames); 1 in epoch mode

@@ -480,6 +480,7 @@ struct Ctx {
     uint32_t tid;
     uint32_t lane;
     uint32_t warp;
+    uint32_t hub_factor;
     Shared* sh;
     uint32_t n;
     bool low_degree;
@@ -522,7 +523,7 @@ __device__ __forceinline__ uint32_t block_inclusive_sum(Ctx& C, uint32_t x, uint
 constexpr unsigned long long kNoTok = ~0ull;
 // Probe passes may pass the other side's last level [l_lo, l_hi) (t-side
 // queue entries when l_t): a frontier vertex whose adjacency is much longer
-// than that list (deg > 4 |L| log2 deg) is not scanned; instead every list
+// than that list (deg > |L| log2 deg, SamplerParams::hub_factor) is not scanned; instead every list
 // vertex is binary-searched in its ascending adjacency (the same edges, found
 // in |L| log deg reads: C5's meeting probes are dominated by a few hubs
 // against ~1k-vertex levels). body runs once per found edge, as for scanned ones.
@@ -535,8 +536,10 @@ __device__ __forceinline__ bool hub_search(const Ctx& C, uint32_t o, uint32_t e,
     }
     return l < e && C.N(l) == v;
 }
-__device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list) {
-    return ADSB_HUB_PROBE && list && deg > 4u * list * (32u - __clz(deg));
+// factor in quarters: deg > (factor / 4) |L| log2 deg
+__device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list, uint32_t factor) {
+    return ADSB_HUB_PROBE && list && factor &&
+           4ull * deg > static_cast<unsigned long long>(factor) * list * (32u - __clz(deg));
 }
 // The chunk's hubs against the level list: pair (h, j) per thread, one binary
 // search each. The hub list is complete (filled before the chunk's scan barrier).
@@ -663,7 +666,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             slot = S.find(u, meta);
             val = prep(slot, meta, e - o);
             scanned = e - o;
-            if (is_hub(e - o, l_hi - l_lo)) {
+            if (is_hub(e - o, l_hi - l_lo, C.hub_factor)) {
                 const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
                 if (h < kMaxHubs) {
                     sh.hub_o[h] = o;
@@ -750,7 +753,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             uint32_t meta;
             slot = S.find(u, meta);
             val = prep(slot, meta, deg);
-            if (is_hub(deg, l_hi - l_lo)) {
+            if (is_hub(deg, l_hi - l_lo, C.hub_factor)) {
                 const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
                 if (h < kMaxHubs) {
                     sh.hub_o[h] = o;
@@ -1940,6 +1943,7 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
     C.pol = csr_policy(p.csr_hint);
 #endif
     C.tid = threadIdx.x;
+    C.hub_factor = p.hub_factor;
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;
