@@ -82,17 +82,24 @@ __global__ void uf_link_round(const uint32_t* __restrict__ off, const uint32_t* 
 // The most frequent root among 256 evenly spaced vertices (one block).
 __global__ void uf_sample_mode(uint32_t* parent, uint32_t n, uint32_t* mode) {
     __shared__ uint32_t roots[256];
-    __shared__ unsigned long long best;
+    __shared__ unsigned long long wbest[8];
     const uint32_t i = threadIdx.x;
     const uint32_t v = static_cast<uint32_t>((static_cast<uint64_t>(i) * n) / 256);
     roots[i] = uf_root<false>(parent, min(v, n - 1));
-    if (i == 0) best = 0;
     __syncthreads();
     uint32_t count = 0;
     for (uint32_t j = 0; j < 256; ++j) count += roots[j] == roots[i] ? 1u : 0u;
-    atomicMax(&best, (static_cast<unsigned long long>(count) << 32) | roots[i]);
+    // max of (count, root) by warp shuffles, then over the 8 warps (no 64-bit
+    // shared atomics: they are CAS loops on sm_100)
+    unsigned long long key = (static_cast<unsigned long long>(count) << 32) | roots[i];
+    for (int d = 16; d; d >>= 1) key = max(key, __shfl_xor_sync(0xFFFFFFFFu, key, d));
+    if ((i & 31) == 0) wbest[i >> 5] = key;
     __syncthreads();
-    if (i == 0) *mode = static_cast<uint32_t>(best);
+    if (i == 0) {
+        unsigned long long best = 0;
+        for (int w = 0; w < 8; ++w) best = max(best, wbest[w]);
+        *mode = static_cast<uint32_t>(best);
+    }
 }
 
 // The rest of the edges, only for vertices outside the sampled giant tree:

@@ -939,12 +939,29 @@ __device__ uint32_t level_degrees(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bo
 // Result of the BFS phase: distance split d = a + b + 1.
 struct Meet {
     uint32_t a, b;
-    int status;  // 0 met, 1 store overflow (redo on the global store), 2 inconsistent
+    int status;  // 0 met, 1 store overflow (redo on the global store), 2 inconsistent,
+                 // 3 table full at a claim pass (continue on the global store from BfsState)
 };
 
+// Loop state of bfs() between levels: what a sample carries from the
+// shared-memory table to a global region when the table fills up at a claim
+// pass (the completed levels are copied; that level's claims are redone).
+struct BfsState {
+    uint32_t s_lo, s_hi, t_lo, t_hi, a, b, used;
+    unsigned long long deg_s, deg_t;
+};
+
+#ifndef ADSB_MIGRATE
+#define ADSB_MIGRATE 1
+#endif
+
 template <class Store>
-__device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
+__device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nullptr) {
     Shared& sh = *C.sh;
+    // io != nullptr on entry with io->used == ~0u: resume a migrated sample at
+    // the claim pass of its current level (the probe found no meeting there);
+    // on a claim-pass overflow of the table the state is written to io.
+    const bool resume = io != nullptr && io->used == ~0u;
     // Level L = a + b uses counter slot L % 3; thread 0 zeroes slot (L+1) % 3
     // as level L starts: every thread read that slot (as level L-2's) before
     // level L-1's barriers, and level L+1 writes it only after level L's.
@@ -952,6 +969,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     S.set_level(&sh.lvl_ins[2], 0);
     if (C.tid == 0) {
         for (int i = 0; i < 3; ++i) sh.lvl_cnt[i] = sh.lvl_deg[i] = sh.lvl_ins[i] = sh.lvl_met[i] = 0;
+    }
+    if (!resume && C.tid == 0) {
         bool ins;
         uint32_t m;
         const uint32_t ss = S.claim(s, 0u, ins, m);
@@ -978,7 +997,19 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
     const bool by_count = ADSB_LOWDEG_COUNT && C.low_degree && S.room_for(~0ull);
     unsigned long long deg_s = by_count ? 1ull : C.O(s + 1) - C.O(s);
     unsigned long long deg_t = by_count ? 1ull : C.O(t + 1) - C.O(t);
+    bool skip_next = false;
+    if (resume) {
+        s_lo = io->s_lo, s_hi = io->s_hi, t_lo = io->t_lo, t_hi = io->t_hi, a = io->a, b = io->b, used = 0;
+        deg_s = io->deg_s, deg_t = io->deg_t;
+        skip_next = true;
+    }
+    auto migrate = [&](uint32_t used_now) -> Meet {
+        if (io) *io = BfsState{s_lo, s_hi, t_lo, t_hi, a, b, used_now, deg_s, deg_t};
+        return {a, b, io ? 3 : 1};
+    };
     for (;;) {
+        const bool skip_probe = skip_next;  // first level of a resumed sample: its probe already ran
+        skip_next = false;
         if (a >= Store::kMaxDist || b >= Store::kMaxDist) return {a, b, 1};  // deeper than the store encodes
         const uint32_t cur = (a + b) % 3, nxt = (a + b + 1) % 3;
         if (C.tid == 0) sh.lvl_cnt[nxt] = sh.lvl_deg[nxt] = sh.lvl_ins[nxt] = sh.lvl_met[nxt] = 0;
@@ -1075,6 +1106,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             // ---- s-side level a: probe for the t-ball (meeting level fills sigma of T_b);
             // hubs of the frontier are searched for T_b's vertices instead of scanned
             if (C.tid == 0) sh.st_verts += s_hi - s_lo;
+            if (!skip_probe) {
             for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
                       [&](uint32_t, unsigned long long su, uint32_t v) {
@@ -1088,6 +1120,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       },
                       t_lo, t_hi, true);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
+            }
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
             for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
@@ -1108,7 +1141,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             __syncthreads();  // counters and overflow final before any thread reads them
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
-            if (sh.overflow) return {a, b, 1};
+            if (sh.overflow) return migrate(used);
             if (!S.pre_zeroed())
             for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
@@ -1127,6 +1160,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
         } else {
             // ---- t-side level b: probe for the s-ball (hubs searched for S_a's vertices)
             if (C.tid == 0) sh.st_verts += t_hi - t_lo;
+            if (!skip_probe) {
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
                       [&](uint32_t su_slot, unsigned long long, uint32_t v) {
@@ -1140,6 +1174,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
                       },
                       s_lo, s_hi, false);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
+            }
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
                       [&](uint32_t, uint32_t, uint32_t) { return 0ull; },
@@ -1157,7 +1192,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t) {
             __syncthreads();
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.t_cnt = min(t_hi + added, S.qcap);
-            if (sh.overflow) return {a, b, 1};
+            if (sh.overflow) return migrate(used);
             t_lo = t_hi;
             t_hi += added;
             used += sh.lvl_ins[cur];
@@ -1643,7 +1678,7 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
 // store), 2 inconsistent state.
 template <int kMode, class Store>
 __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t s, uint32_t t,
-                          uint32_t frame_local) {
+                          uint32_t frame_local, BfsState* io = nullptr) {
     Shared& sh = *C.sh;
     S.begin(C.tid);
     if (C.tid == 0) {
@@ -1651,7 +1686,8 @@ __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
     }
     __syncthreads();
     ADSB_PHASE_MARK(t0);
-    const Meet mt = bfs(C, S, s, t);
+    const Meet mt = bfs(C, S, s, t, io);
+    if (mt.status == 3) return 3;  // table kept intact for migrate_to_global
     ADSB_PHASE_MARK(t1);
     ADSB_PHASE_ADD(0, t1 - t0);
     ADSB_PHASE_ADD(5, mt.a + mt.b + 1);
@@ -1762,6 +1798,38 @@ __device__ void release_region(const SamplerParams& p, uint32_t region, uint32_t
                  : "memory");
 }
 
+// A sample whose shared-memory table filled up at a claim pass continues on a
+// global region instead of being redone: the completed levels (s-side dist
+// <= a, t-side dist <= b: vertex, side, dist, DAG flag, sigma), both queue
+// ends and the level boundaries are copied; the partial claims of the failed
+// level are dropped (its claim pass reruns on the region). Then the table is
+// cleared for the membership filter. Results are unchanged: the region holds
+// exactly the state the global store would have built.
+template <bool kVec, class GS>
+__device__ void migrate_to_global(Ctx& C, const SamplerParams& p, GS& gs, const BfsState& st) {
+    Shared& sh = *C.sh;
+    auto sm = make_smem_store<kVec>(p, sh);
+    const unsigned long long hi_word = gs.clear ? GS::kPresent : static_cast<unsigned long long>(gs.tag) << 32;
+    for (uint32_t h = C.tid; h < sm.cap; h += kBT) {
+        const uint32_t w = sm.km[h];
+        if (w == 0u) continue;
+        const uint32_t meta = SmemStoreT<kVec>::decode(w);
+        const bool keep = m_is_t(meta) ? m_dist(meta) <= st.b : m_dist(meta) <= st.a;
+        if (!keep) continue;
+        const uint32_t v = (w >> 8) - 1u;
+        __stcg(gs.st + 2ull * v, hi_word | meta);
+        __stcg(gs.st + 2ull * v + 1, sm.sig[h]);
+    }
+    for (uint32_t i = C.tid; i < st.s_hi; i += kBT) __stcg(gs.qv + i, sm.qv[i]);
+    for (uint32_t j = C.tid; j < st.t_hi; j += kBT) __stcg(gs.qv + gs.tpos(j), sm.qv[sm.tpos(j)]);
+    for (uint32_t k = C.tid; k <= st.b + 1 && k < kSmemLevels; k += kBT) gs.tlev[k] = sh.tlev_small[k];
+    for (uint32_t k = C.tid; k <= st.a + 1 && k < kSmemLevels; k += kBT) gs.slev[k] = sh.slev_small[k];
+    __threadfence_block();
+    __syncthreads();
+    sm.clear_all(C.tid);
+    __syncthreads();
+}
+
 // gtag: the global-only kernel's generation tag for its own region (block-uniform).
 template <int kMode, bool kGlobalOnly, bool kVec>
 __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint32_t frame_local, uint32_t& gtag) {
@@ -1772,15 +1840,21 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
     if (__ldg(p.label + s) != __ldg(p.label + t)) return;  // disconnected pair: empty sample
     ADSB_PHASE_MARK(os0);
     int rc = 1;
+    BfsState mig{};
+    mig.used = 0;
     if constexpr (!kGlobalOnly) {
         if (p.use_smem) {
             auto sm = make_smem_store<kVec>(p, *C.sh);
-            rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local);
+            // with the membership filter available, a table overflow at a claim
+            // pass migrates the sample (rc 3) instead of redoing it from scratch
+            const bool can_migrate = ADSB_MIGRATE && ADSB_FALLBACK_FILTER &&
+                                     p.hash_cap * 12u >= (1u << GlobalStoreT<ADSB_LOAD_BATCH>::kFiltLog) / 8u;
+            rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local, can_migrate ? &mig : nullptr);
         }
     }
-    const bool fell_back = rc == 1;
+    const bool fell_back = rc == 1 || rc == 3;
     (void)fell_back;
-    if (rc == 1) {
+    if (rc == 1 || rc == 3) {
         uint32_t region = blockIdx.x, tag;
         if constexpr (kGlobalOnly) {
             tag = ++gtag;
@@ -1807,14 +1881,27 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             if constexpr (kGlobalOnly) gtag = 1;
         }
         auto gs = make_global_store<kGlobalOnly>(p, region, tag);
+        if constexpr (!kGlobalOnly) {
+            if (rc == 3) migrate_to_global<kVec>(C, p, gs, mig);
+        }
 #if ADSB_FALLBACK_FILTER
-        // the table is empty here (the overflowed attempt cleared it) and
-        // covers the filter: 2^18 bits = 32 KB <= hash_cap * 12 B
+        // the table is empty here (the overflowed attempt cleared it, or the
+        // migration did) and covers the filter: 2^18 bits = 32 KB <= hash_cap * 12 B
         if constexpr (!kGlobalOnly)
-            if (p.hash_cap * 12u >= (1u << GlobalStoreT<ADSB_LOAD_BATCH>::kFiltLog) / 8u)
+            if (p.hash_cap * 12u >= (1u << GlobalStoreT<ADSB_LOAD_BATCH>::kFiltLog) / 8u) {
                 gs.filt = reinterpret_cast<uint32_t*>(adsb_dyn);
+                if (rc == 3) {
+                    // the filter holds exactly the migrated (claimed) vertices
+                    for (uint32_t i = C.tid; i < mig.s_hi + mig.t_hi; i += kBT) {
+                        const uint32_t q = i < mig.s_hi ? i : gs.tpos(i - mig.s_hi);
+                        gs.fset(__ldcg(gs.qv + q));
+                    }
+                    __syncthreads();
+                }
+            }
 #endif
-        rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local);
+        if (rc == 3) mig.used = ~0u;  // resume at the claim pass
+        rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local, rc == 3 ? &mig : nullptr);
         if constexpr (!kGlobalOnly) {
             __syncthreads();  // every thread is done with the region
             if (C.tid == 0) release_region(p, region, tag);

@@ -1,8 +1,15 @@
 # Round 2 profiles: bench lines (C5 default + C1..C4), launch list of the default bench, ncu --set full (+ L2 bytes)
 # of the sampler kernel on every config. Each ncu command follows the same plain command (exit 0) with &&.
-mkdir -p gpurun_out/r2p; rm -f gpurun_out/r2p/*
+# Reports go to /tmp/ncu (gpurun_out is capped at 64 MiB); their summaries and the C5 report come back.
+mkdir -p gpurun_out/r2p /tmp/ncu; rm -f gpurun_out/r2p/*
 export ADSB_GRAPH_CACHE=build/gcache
 M="--metrics lts__t_bytes.sum,lts__t_sectors.sum,lts__t_sector_hit_rate.pct"
+for c in c5_rmat24 c2_rmat18 c3_ba c4_grid c1_er; do timeout 300 python -c "
+import sys; sys.path.insert(0,'.')
+from paper_1903_09422_b200 import datasets; datasets.graph('$c')" ; done
+if [ -f ab/libadsb_phase.so ]; then
+  ADSB_LIB_PATH=ab/libadsb_phase.so ADSB_TRACE=1 timeout 300 python scripts/prof_one.py c5_rmat24 2 > gpurun_out/r2p/phase_c5.log 2>&1
+fi
 timeout 1500 python bench.py --steps 10 --warmup 3 > gpurun_out/r2p/bench_c5.log 2>&1
 for c in c1_er c2_rmat18 c3_ba; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/r2p/bench_$c.log 2>&1; done
 timeout 900 python bench.py --config c4_grid --steps 2 --warmup 3 > gpurun_out/r2p/bench_c4_grid.log 2>&1
@@ -14,14 +21,19 @@ timeout 1500 ncu --set full $M --clock-control none --import-source on -k regex:
   -o gpurun_out/r2p/c5_full python scripts/prof_capped.py c5_rmat24 64 > gpurun_out/r2p/ncu_c5.log 2>&1
 timeout 300 python scripts/prof_one.py c2_rmat18 2 > gpurun_out/r2p/plain_c2.log 2>&1 && \
 timeout 900 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -s 1 -c 1 \
-  -o gpurun_out/r2p/c2_full python scripts/prof_one.py c2_rmat18 2 > gpurun_out/r2p/ncu_c2.log 2>&1
+  -o /tmp/ncu/c2_full python scripts/prof_one.py c2_rmat18 2 > gpurun_out/r2p/ncu_c2.log 2>&1
 timeout 300 python scripts/prof_one.py c3_ba 1 > gpurun_out/r2p/plain_c3.log 2>&1 && \
 timeout 900 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -s 2 -c 1 \
-  -o gpurun_out/r2p/c3_full python scripts/prof_one.py c3_ba 1 > gpurun_out/r2p/ncu_c3.log 2>&1
+  -o /tmp/ncu/c3_full python scripts/prof_one.py c3_ba 1 > gpurun_out/r2p/ncu_c3.log 2>&1
 timeout 300 python scripts/prof_one.py c1_er 1 > gpurun_out/r2p/plain_c1.log 2>&1 && \
 timeout 900 ncu --set full $M --clock-control none -k regex:sampler_kernel -c 1 \
-  -o gpurun_out/r2p/c1_full python scripts/prof_one.py c1_er 1 > gpurun_out/r2p/ncu_c1.log 2>&1
+  -o /tmp/ncu/c1_full python scripts/prof_one.py c1_er 1 > gpurun_out/r2p/ncu_c1.log 2>&1
 timeout 600 python scripts/prof_capped.py c4_grid 1184 > gpurun_out/r2p/plain_c4.log 2>&1 && \
 timeout 1500 ncu --set full $M --clock-control none -k regex:sampler_cta_kernel -c 1 \
-  -o gpurun_out/r2p/c4_full python scripts/prof_capped.py c4_grid 1184 > gpurun_out/r2p/ncu_c4.log 2>&1
+  -o /tmp/ncu/c4_full python scripts/prof_capped.py c4_grid 1184 > gpurun_out/r2p/ncu_c4.log 2>&1
+for c in c1 c2 c3 c4; do
+  [ -f /tmp/ncu/${c}_full.ncu-rep ] && python scripts/ncu_summary.py /tmp/ncu/${c}_full.ncu-rep > gpurun_out/r2p/${c}_full.json 2>&1
+  [ -f /tmp/ncu/${c}_full.ncu-rep ] && ncu -i /tmp/ncu/${c}_full.ncu-rep --page raw --csv > gpurun_out/r2p/${c}_raw.csv 2>&1
+done
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2p/smoke.log 2>&1
+du -sh gpurun_out/r2p > gpurun_out/r2p/du.txt

@@ -1,6 +1,6 @@
 """Merge one ncu --set full capture of the sampler kernel into profiles/ncu_sampler_summary.json.
 
-    python scripts/ncu_to_summary.py CONFIG REPORT.ncu-rep SAMPLES_IN_LAUNCH "source note"
+    python scripts/ncu_to_summary.py CONFIG REPORT.ncu-rep|RAW.csv SAMPLES_IN_LAUNCH "source note"
 
 Per launch: DRAM bytes (read + write) and L2 bytes (lts__t_bytes), converted
 to bytes per sample, which bench.py scales by the samples a step draws.
@@ -19,7 +19,11 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def metrics(rep: str) -> dict:
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep, or the `ncu -i REP --page raw --csv` output saved on the GPU box"""
+    if rep.endswith(".csv"):
+        txt = Path(rep).read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, row = rows[0], rows[1], rows[2]
     out = {"kernel": row[hdr.index("Kernel Name")]}
