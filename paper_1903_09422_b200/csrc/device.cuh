@@ -121,6 +121,7 @@ struct SamplerArena {
     int kind = 1;            // SamplerKind (0 warp teams, 1 block teams)
     uint32_t hash_cap = 0;   // block teams: shared-memory hash capacity
     uint32_t block_threads = 256;
+    bool vec4 = false;       // blocks sized for the vector kernels' dynamic shared memory
     int layout = 0;          // block teams' global state: 1 cleared (low-degree graphs), 0 tagged
     uint32_t slots = 0;      // warp teams; block teams: global-state regions
     uint32_t blocks = 0;     // block teams: resident blocks launched by the shared-memory kernels

@@ -186,6 +186,16 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     if (const char* e = std::getenv("ADSB_BLOCK")) block_threads = std::strtoul(e, nullptr, 10) == 128 ? 128 : 256;
     if (hash_cap < 64 || hash_cap % 64) invalid("ADSB_HASH_CAP must be a multiple of 64");
     const int k = kind == SamplerKind::kWarp ? 0 : 1;
+    // vectorised adjacency reads where the CSR misses L2 (C5: -2.4%); on an
+    // L2-resident CSR the scalar loop is faster (C2 -7%, C3 -10%). The vector
+    // kernels use 2 KB more dynamic shared memory (blocks per SM below).
+    bool vec4 = false;
+    {
+        int l2 = 0;
+        ADSB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx.device));
+        vec4 = k == 1 && 4ull * (ctx.graph.n + 1) + 4ull * ctx.graph.nnz > static_cast<uint64_t>(l2);
+        if (const char* e = std::getenv("ADSB_VEC4")) vec4 = k == 1 && std::strtoul(e, nullptr, 10) != 0;
+    }
     DeviceRuntime& rt = *ctx.rt;
     rt.active = k;
     std::unique_ptr<SamplerArena>& slot = rt.arena[k];
@@ -194,7 +204,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     // layout's leftovers after a switch, so the state is zeroed then.
     const int layout = k == 1 && ctx.graph.max_degree <= 32 && !std::getenv("ADSB_TAGGED") ? 1 : 0;
     if (slot && slot->n >= n && slot->level_cap >= level_cap && slot->hash_cap == hash_cap &&
-        slot->block_threads == block_threads) {
+        slot->block_threads == block_threads && slot->vec4 == vec4) {
         if (slot->layout != layout) {
             ADSB_CUDA(cudaMemsetAsync(slot->state.ptr, 0, slot->state.bytes(), rt.stream));
             ADSB_CUDA(cudaMemsetAsync(slot->slot_tag.ptr, 0, slot->slot_tag.bytes(), rt.stream));
@@ -209,7 +219,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     ADSB_CUDA(cudaSetDevice(ctx.device));
     const int sms = num_sms(ctx.device);
     const int per_sm = kind == SamplerKind::kWarp ? std::max(sampler_warps_per_sm(true), 8)
-                                                  : std::max(sampler_cta_blocks_per_sm(hash_cap, block_threads), 1);
+                                                  : std::max(sampler_cta_blocks_per_sm(hash_cap, block_threads, vec4), 1);
     size_t free_b = 0, total_b = 0;
     ADSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     // per region: state (16 B/vertex), queue (4), warp teams also ranges (8)
@@ -232,6 +242,7 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->kind = k;
     a->hash_cap = hash_cap;
     a->block_threads = block_threads;
+    a->vec4 = vec4;
     a->layout = layout;
     a->slots = static_cast<uint32_t>(slots);
     // Block teams launch every resident block for the shared-memory kernels
@@ -280,13 +291,10 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
         const uint64_t csr = 4ull * (ctx.graph.n + 1) + 4ull * ctx.graph.nnz;
         p.csr_hint = csr * 2 <= static_cast<uint64_t>(l2) ? 1.0f : 0.0f;
         if (const char* e = std::getenv("ADSB_CSR_HINT")) p.csr_hint = std::strtof(e, nullptr);
-        // vectorised adjacency reads where the CSR misses L2 (C5: -1%); on an
-        // L2-resident CSR the scalar loop is faster (C2 -7%, C3 -10%)
-        p.vec4 = csr > static_cast<uint64_t>(l2) ? 1u : 0u;
+        p.vec4 = a.vec4 ? 1u : 0u;  // chosen with the arena (ensure_arena)
         // hub probes when deg > (hub_factor / 4) |L| log2 deg: 1.0 beat 0.5-4 (C5 -1%, C2 -5% vs 4.0)
         p.hub_factor = 4;
         if (const char* e = std::getenv("ADSB_HUB_FACTOR")) p.hub_factor = std::strtoul(e, nullptr, 10);
-        if (const char* e = std::getenv("ADSB_VEC4")) p.vec4 = std::strtoul(e, nullptr, 10) ? 1u : 0u;
     }
     p.dagq = a.dagq.ptr;
     p.slot_tag = a.slot_tag.ptr;

@@ -104,7 +104,7 @@ int sampler_warps_per_sm(bool deterministic);
 void launch_sampler_warp(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 // Block-team sampler with shared-memory state (sampler_cta.cu): slots = blocks.
 size_t sampler_cta_smem_bytes(uint32_t hash_cap, bool vec4);
-int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads);
+int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads, bool vec4);
 void launch_sampler_cta(bool deterministic, const SamplerParams& p, cudaStream_t stream);
 int sampler_global_blocks_per_sm();
 // single-launch epoch pipeline with device-side folding and stopping (block teams)

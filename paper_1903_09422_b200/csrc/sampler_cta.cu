@@ -158,12 +158,15 @@ void configure_once() {
 }
 }  // namespace
 
-int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads) {
+int sampler_cta_blocks_per_sm(uint32_t hash_cap, uint32_t block_threads, bool vec4) {
     configure_once();
-    const size_t dyn = sampler_cta_smem_bytes(hash_cap, false);
+    const bool v = vec4 && block_threads == 256;
+    const size_t dyn = sampler_cta_smem_bytes(hash_cap, v);
     int blocks = 0;
     if (block_threads == 128)
         ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt128::sampler_cta_kernel<kModeDet, false>, 128, dyn));
+    else if (v)
+        ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet, false, true>, 256, dyn));
     else
         ADSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, bt256::sampler_cta_kernel<kModeDet, false>, 256, dyn));
     return blocks;
