@@ -112,6 +112,11 @@ struct DeviceGraph {
     uint32_t max_degree = 0;
     DevBuf<uint32_t> offsets;  // n+1 (nnz < 2^32 on the device path)
     DevBuf<uint32_t> nbrs;     // nnz
+    // search trees over the rows of high-degree vertices (hub_index.cuh), built
+    // on the first estimate for this handle: hub_ref[v] = word offset of v's
+    // tree in hub_keys (meaningful only where hub_has_tree(deg v))
+    DevBuf<uint32_t> hub_ref;
+    DevBuf<uint32_t> hub_keys;
 };
 
 // Per-(graph, device) sampler scratch: one "slot" per concurrently running
@@ -134,6 +139,7 @@ struct SamplerArena {
     DevBuf<uint32_t> dagq;             // block teams: slots * n t-side DAG lists (push rebuild, low-degree graphs)
     DevBuf<uint32_t> slot_tag;         // slots: generation tag of each region
     DevBuf<uint32_t> slot_busy;        // block teams: bitmap of regions lent to blocks
+    DevBuf<uint32_t> join_bits;        // block teams: slots * ceil(n / 32) vertex bitmaps of the join levels
 };
 
 // Process-wide per-device runtime shared by every graph handle on that
@@ -172,6 +178,7 @@ struct DeviceContext {
     DevBuf<uint32_t> labels;  // component labels (reference numbering)
     bool labels_ready = false;
     bool dub_ready = false;   // the graph is immutable: labels and D_ub are computed once per handle
+    bool hub_ready = false;   // hub search trees built (or found unnecessary)
     int use_smem = -1;        // block teams: -1 undecided, 0 global-store-only, 1 shared-memory table first
     uint64_t diameter_bound = 0;
     uint32_t num_components = 0;
@@ -203,6 +210,9 @@ uint32_t device_components(DeviceContext& ctx);
 uint64_t device_eccentricity(DeviceContext& ctx, uint32_t source);
 // graph.hpp:202-214 diameter_upper_bound (requires device_components first)
 uint64_t device_diameter_bound(DeviceContext& ctx);
+
+// search trees over high-degree adjacency rows (hub_index.cu), once per handle
+void device_hub_index(DeviceContext& ctx);
 
 // exact normalised BC (Brandes, f64; brandes.cu); returns the kernel time in ms
 double device_exact_bc(DeviceContext& ctx, double* host_bc);
