@@ -194,12 +194,6 @@ adsb_status adsb_sample_frames(const adsb_graph *g, int device, uint64_t seed, u
                                uint64_t first, uint64_t count, uint64_t *frame_offsets,
                                uint32_t *incs, uint64_t cap);
 
-/* Diagnostic counters of the block sampler's join levels on `device` since the
- * last reset: out = {attempts, joined, empty joins, joins too large for the
- * shared-memory table} ("Join levels"). The parity tests use them
- * to prove that the joined path ran. No reference counterpart. */
-adsb_status adsb_sampler_counters(int device, uint64_t out[4], int reset);
-
 /* ---- validation: exact BC on the device (Brandes, f64) ---------------------- */
 /* Exact betweenness of every vertex, normalised by n(n-1) like estimate_bc's
  * scores: the check the reference makes against ApspOracle / Brandes

@@ -138,7 +138,6 @@ _SIGS = {
     "adsb_kadabra_check": (C.c_int, [u64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.POINTER(C.c_int)]),
     "adsb_estimate_bc": (C.c_int, [P, C.c_double, C.c_double, C.POINTER(Config), dblp, u64p, C.POINTER(Stats)]),
     "adsb_exact_bc": (C.c_int, [P, C.c_int, dblp, dblp]),
-    "adsb_sampler_counters": (C.c_int, [C.c_int, u64p, C.c_int]),
     "adsb_sample_frames": (C.c_int, [P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u64p, u32p, C.c_uint64]),
     "adsb_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "adsb_comm_init": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(P)]),

@@ -25,8 +25,6 @@ struct adsb_graph {
 
 namespace adsb {
 
-void sampler_join_counters(unsigned long long out[4], bool reset);  // sampler_cta.cu
-
 namespace {
 thread_local std::string g_last_error;
 
@@ -413,16 +411,6 @@ adsb_status adsb_exact_bc(const adsb_graph* g, int device, double* bc, double* d
         Locked L = locked_context(g, device);
         const double ms = device_exact_bc(L.ctx, bc);
         if (device_ms) *device_ms = ms;
-    });
-}
-
-adsb_status adsb_sampler_counters(int device, uint64_t out[4], int reset) {
-    return guard([&] {
-        need(out, "out");
-        ADSB_CUDA(cudaSetDevice(device < 0 ? 0 : device));
-        unsigned long long h[4] = {};
-        sampler_join_counters(h, reset != 0);
-        for (int i = 0; i < 4; ++i) out[i] = h[i];
     });
 }
 

@@ -113,8 +113,8 @@ struct DeviceGraph {
     DevBuf<uint32_t> offsets;  // n+1 (nnz < 2^32 on the device path)
     DevBuf<uint32_t> nbrs;     // nnz
     // search trees over the rows of high-degree vertices (hub_index.cuh), built
-    // on the first estimate for this handle: hub_ref[v] = word offset of v's
-    // tree in hub_keys (meaningful only where hub_has_tree(deg v))
+    // on the first estimate for this handle when the CSR misses L2: hub_ref[v] =
+    // word offset of v's tree in hub_keys (meaningful only where hub_has_tree(deg v))
     DevBuf<uint32_t> hub_ref;
     DevBuf<uint32_t> hub_keys;
 };
@@ -139,7 +139,6 @@ struct SamplerArena {
     DevBuf<uint32_t> dagq;             // block teams: slots * n t-side DAG lists (push rebuild, low-degree graphs)
     DevBuf<uint32_t> slot_tag;         // slots: generation tag of each region
     DevBuf<uint32_t> slot_busy;        // block teams: bitmap of regions lent to blocks
-    DevBuf<uint32_t> join_bits;        // block teams: slots * ceil(n / 32) vertex bitmaps of the join levels
 };
 
 // Process-wide per-device runtime shared by every graph handle on that

@@ -259,11 +259,6 @@ void ensure_arena(DeviceContext& ctx, uint32_t level_cap) {
     a->slot_tag.alloc(slots);
     a->slot_busy.alloc((slots + 31) / 32);
     ADSB_CUDA(cudaMemsetAsync(a->slot_busy.ptr, 0, a->slot_busy.bytes(), rt.stream));
-    if (kind == SamplerKind::kBlock) {
-        // one bit per vertex and region (1/128 of the state): zero between uses
-        a->join_bits.alloc(slots * ((static_cast<uint64_t>(cap_n) + 31) / 32));
-        ADSB_CUDA(cudaMemsetAsync(a->join_bits.ptr, 0, a->join_bits.bytes(), rt.stream));
-    }
     ADSB_CUDA(cudaMemsetAsync(a->state.ptr, 0, a->state.bytes(), rt.stream));
     ADSB_CUDA(cudaMemsetAsync(a->slot_tag.ptr, 0, a->slot_tag.bytes(), rt.stream));
     ADSB_CUDA(cudaStreamSynchronize(rt.stream));
@@ -297,8 +292,10 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
         p.csr_hint = csr * 2 <= static_cast<uint64_t>(l2) ? 1.0f : 0.0f;
         if (const char* e = std::getenv("ADSB_CSR_HINT")) p.csr_hint = std::strtof(e, nullptr);
         p.vec4 = a.vec4 ? 1u : 0u;  // chosen with the arena (ensure_arena)
-        // hub probes when deg > (hub_factor / 4) |L| log2 deg: 1.0 beat 0.5-4 (C5 -1%, C2 -5% vs 4.0)
-        p.hub_factor = 4;
+        // hub probes when deg > (hub_factor / 4) |L| cost(deg), cost = dependent loads of one
+        // search: 1.0 beat 0.5-4 with plain binary searches (C5 -1%, C2 -5% vs 4.0); with
+        // search trees (cost ~ log2(deg) / 3 + 1) 3.0 beat 1-2 and equals 4 (profiles/r02_ab_hub_trees.txt)
+        p.hub_factor = a.vec4 && !std::getenv("ADSB_NO_HUB_TREES") ? 12 : 4;
         if (const char* e = std::getenv("ADSB_HUB_FACTOR")) p.hub_factor = std::strtoul(e, nullptr, 10);
     }
     p.dagq = a.dagq.ptr;
@@ -306,25 +303,16 @@ SamplerParams base_params(DeviceContext& ctx, uint64_t seed, uint64_t spf) {
     p.slot_busy = a.slot_busy.ptr;
     p.blocks = a.blocks;
     p.hash_cap = a.hash_cap;
-    // join levels (hub-heavy graphs only: the cleared layout has no hubs to join over)
-    {
-        const char* e = std::getenv("ADSB_JOIN");
-        p.join_bits = a.layout == 0 && !(e && e[0] == '0') ? a.join_bits.ptr : nullptr;
-    }
-    p.join_words = (a.n + 31) / 32;
-    if (a.kind == 1 && !std::getenv("ADSB_NO_HUB_TREES")) {
+    // Hub search trees where the CSR misses L2 (the vector kernels, chosen by
+    // the same test): a search's dependent loads are HBM round trips there. On
+    // an L2-resident CSR the plain binary search is as fast (C2 +4% with trees).
+    if (a.kind == 1 && a.vec4 && !std::getenv("ADSB_NO_HUB_TREES")) {
         device_hub_index(ctx);  // once per handle
         if (ctx.graph.hub_keys.ptr) {
             p.hub_ref = ctx.graph.hub_ref.ptr;
             p.hub_keys = ctx.graph.hub_keys.ptr;
         }
     }
-    // bulk L2 prefetch of scanned rows: only where the CSR misses L2 (vec4 is chosen by the same test)
-    p.nnz = static_cast<uint32_t>(ctx.graph.nnz);
-    p.bulk_min = a.vec4 ? 64u : 0u;
-    if (const char* e = std::getenv("ADSB_BULK_MIN")) p.bulk_min = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
-    p.join_factor = 4;
-    if (const char* e = std::getenv("ADSB_JOIN_FACTOR")) p.join_factor = static_cast<uint32_t>(std::strtoul(e, nullptr, 10));
     p.use_smem = ctx.use_smem == 1 ? 1u : 0u;
     p.global_grid = static_cast<uint32_t>(num_sms(ctx.device) * std::max(sampler_global_blocks_per_sm(), 1));
     // Low-degree graphs (cleared layout): fewer, wider teams. Half the samples
@@ -925,7 +913,6 @@ EngineOutput estimate_bc(DeviceContext& ctx, double eps, double delta, const Eng
         std::fprintf(stderr, "[adsb] results at %.3f ms (pre %.3f ms)\n", 1e3 * out.ads_seconds,
                      1e3 * out.preprocess_seconds);
         sampler_phase_report();
-        sampler_join_report();
     }
     return out;
 }

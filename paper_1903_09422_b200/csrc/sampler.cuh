@@ -78,15 +78,9 @@ struct SamplerParams {
     uint32_t* slot_tag;         // slots
     uint32_t* slot_busy;        // block teams: region bitmap (fallback samples borrow a region)
     uint32_t blocks;            // block teams: shared-memory kernel grid
-    // join levels (sampler_cta_body.cuh join_level): one vertex bitmap per region
-    uint32_t* join_bits;        // slots * join_words, all-zero between uses (nullptr: joins off)
-    uint32_t join_words;        // words per region (>= ceil(n / 32))
-    // hub search trees (hub_index.cuh); nullptr: plain binary searches
+    // hub search trees (hub_index.cuh), used by the vector kernels; nullptr: plain binary searches
     const uint32_t* hub_ref;
     const uint32_t* hub_keys;
-    uint32_t bulk_min;          // block teams: bulk-prefetch scanned rows of >= this many entries into L2 (0: off)
-    uint32_t nnz;               // adjacency entries (bounds of the bulk prefetch)
-    uint32_t join_factor;       // skip a claim pass whose adjacency exceeds join_factor x the table's room (0: never)
     // deterministic output: (v << 32) | frame-in-batch
     unsigned long long* events;
     unsigned long long* ev_cursor;
@@ -120,10 +114,6 @@ int sampler_global_blocks_per_sm();
 void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream);
 // diagnostic builds (-DADSB_PHASE_TIMING): print and reset per-phase cycle sums
 void sampler_phase_report();
-// ADSB_TRACE: print and reset the join-level counters (attempts, joined, empty, too large)
-void sampler_join_report();
-// the same counters for the C ABI's diagnostic entry point (adsb_sampler_counters)
-void sampler_join_counters(unsigned long long out[4], bool reset);
 
 enum class SamplerKind { kWarp, kBlock };
 SamplerKind sampler_kind();  // ADSB_SAMPLER=warp|block (default block)

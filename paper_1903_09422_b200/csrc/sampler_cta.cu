@@ -68,15 +68,6 @@ __device__ unsigned long long adsb_phase[16];
     } while (0)
 #endif
 
-// Join-level counters (sampler_cta_body.cuh join_level): attempts, joined,
-// empty joins, joins too large for the table. One atomic per attempt by
-// thread 0; printed under ADSB_TRACE.
-__device__ unsigned long long adsb_join_ctr[4];
-#define ADSB_JOIN_COUNT(i)                                        \
-    do {                                                          \
-        if (threadIdx.x == 0) atomicAdd(&adsb_join_ctr[i], 1ull); \
-    } while (0)
-
 #ifdef ADSB_DEBUG_CHECKS
 #include <cstdio>
 #define ADSB_DCHECK(cond, ...)                                                              \
@@ -237,23 +228,6 @@ void launch_sampler_fused(const SamplerParams& p, cudaStream_t stream) {
     else if (p.vec4) bt256::sampler_cta_kernel<kModeFused, false, true><<<p.blocks, 256, dyn, stream>>>(p);
     else bt256::sampler_cta_kernel<kModeFused, false><<<p.blocks, 256, dyn, stream>>>(p);
     ADSB_CUDA(cudaGetLastError());
-}
-
-void sampler_join_counters(unsigned long long out[4], bool reset) {
-    ADSB_CUDA(cudaDeviceSynchronize());
-    ADSB_CUDA(cudaMemcpyFromSymbol(out, adsb_join_ctr, 4 * sizeof(unsigned long long)));
-    if (reset) {
-        const unsigned long long z[4] = {};
-        ADSB_CUDA(cudaMemcpyToSymbol(adsb_join_ctr, z, sizeof(z)));
-    }
-}
-
-void sampler_join_report() {
-    unsigned long long h[4] = {};
-    sampler_join_counters(h, true);
-    if (h[0])
-        std::fprintf(stderr, "[adsb] join levels: %llu attempts, %llu joined, %llu empty, %llu too large\n", h[0], h[1],
-                     h[2], h[3]);
 }
 
 void sampler_phase_report() {

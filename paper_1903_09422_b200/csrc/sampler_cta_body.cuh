@@ -79,6 +79,7 @@ template <bool kVec>
 struct SmemStoreT {
     static constexpr uint32_t kLoadBatch = ADSB_LOAD_BATCH;
     static constexpr bool kVec4 = kVec;  // flattened adjacency read as 16-byte vectors
+    static constexpr bool kTrees = kVec; // hub searches go through the search trees (hub_index.cuh)
     // vectorised reads: each chunk vertex's adjacency range [off(u), off(u+1))
     // as lo[kBT] then hi[kBT], in dynamic shared memory (vector kernels only:
     // a larger static block would shrink the L1 the scalar kernels prefetch into)
@@ -264,8 +265,6 @@ struct SmemStoreT {
     __device__ bool room_for(unsigned long long edges) const {
         return ins_base < limit && edges <= limit - ins_base;
     }
-    // insertions the table still takes after `used` (join-level prediction)
-    __device__ uint32_t join_room(uint32_t used) const { return used < limit ? limit - used : 0u; }
 };
 using SmemStore = SmemStoreT<false>;
 
@@ -312,10 +311,11 @@ using SmemStore = SmemStoreT<false>;
 #ifndef ADSB_LOWDEG_COUNT
 #define ADSB_LOWDEG_COUNT 1
 #endif
-template <uint32_t kU, bool kBatch = false>
+template <uint32_t kU, bool kBatch = false, bool kTr = false>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
     static constexpr bool kVec4 = false;
+    static constexpr bool kTrees = kTr;  // fallback samples of the vector kernels
     static constexpr bool kBatchClaims = kBatch;  // global-store-only kernels
     static constexpr bool kSlotIsVertex = true;   // find() returns the vertex as its slot
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
@@ -439,7 +439,6 @@ struct GlobalStoreT {
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
     __device__ bool room_for(unsigned long long) const { return filt == nullptr; }
     __device__ void set_level(uint32_t*, uint32_t) {}
-    __device__ uint32_t join_room(uint32_t) const { return 0xFFFFFFFFu; }  // no capacity limit: never predicted
 };
 
 // CSR reads carry an L2 eviction-priority hint: evict_last when the CSR fits
@@ -487,27 +486,10 @@ struct Ctx {
     uint32_t lane;
     uint32_t warp;
     uint32_t hub_factor;
-    uint32_t join_factor;  // 0: no join-level prediction (joins off, or the store has no bitmap)
-    uint32_t bulk_min;     // rows of at least this many entries are bulk-prefetched into L2 before a scan (0: never)
-    uint32_t nnz;
     Shared* sh;
     uint32_t n;
     bool low_degree;
 };
-
-// Bulk L2 prefetch of an adjacency row about to be scanned: one
-// cp.async.bulk.prefetch (UBLKPF.L2) streams the whole row from HBM into L2
-// ahead of the scan's demand loads, whose per-thread chain (one 4- or 16-byte
-// load in flight plus one L1 prefetch) otherwise pays a DRAM round trip per
-// iteration. The range is widened to 16-byte bounds inside the array.
-constexpr uint32_t kBulkMaxBytes = 1u << 20;
-__device__ __forceinline__ void bulk_prefetch_row(const Ctx& C, uint32_t o, uint32_t e) {
-    const uint32_t a = o & ~3u;
-    const uint32_t b = min((e + 3u) & ~3u, C.nnz & ~3u);
-    if (b <= a) return;
-    const uint32_t bytes = min((b - a) * 4u, kBulkMaxBytes);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(C.nbrs + a), "r"(bytes) : "memory");
-}
 
 // Inclusive prefix sum over the block (warp shuffles + per-warp totals, one
 // barrier). sh.wtot is rewritten only after the caller's next barrier.
@@ -551,8 +533,9 @@ constexpr unsigned long long kNoTok = ~0ull;
 // in |L| log deg reads: C5's meeting probes are dominated by a few hubs
 // against ~1k-vertex levels). body runs once per found edge, as for scanned ones.
 // Position of the first entry >= v in the ascending row [o, e) whose search
-// tree starts at `tree` (hub_index.cuh): one 8-key node per level, then a
-// search inside one 32-entry block of the row.
+// tree starts at `tree` (hub_index.cuh): one 8-key node (one sector) per
+// level, then inside one 32-entry block of the row one parallel step over its
+// four 8-entry groups and a search inside one group.
 __device__ __forceinline__ uint32_t tree_lower_bound(const Ctx& C, const uint32_t* __restrict__ tree, uint32_t o,
                                                      uint32_t e, uint32_t v) {
     if (v > __ldg(tree + 7)) return e;
@@ -564,6 +547,11 @@ __device__ __forceinline__ uint32_t tree_lower_bound(const Ctx& C, const uint32_
         pos = pos * kHubFan + c;  // c <= 7: v <= the row's maximum, so every visited node holds a key >= v
     }
     uint32_t l = o + pos * kHubLeaf, r = min(l + kHubLeaf, e);
+    const uint32_t k0 = l + 7 < r ? C.N(l + 7) : 0xFFFFFFFFu;
+    const uint32_t k1 = l + 15 < r ? C.N(l + 15) : 0xFFFFFFFFu;
+    const uint32_t k2 = l + 23 < r ? C.N(l + 23) : 0xFFFFFFFFu;
+    l += 8u * ((k0 < v) + (k1 < v) + (k2 < v));
+    r = min(l + 8u, r);
     while (l < r) {
         const uint32_t mid = (l + r) >> 1;
         if (C.N(mid) < v) l = mid + 1;
@@ -571,27 +559,28 @@ __device__ __forceinline__ uint32_t tree_lower_bound(const Ctx& C, const uint32_
     }
     return l;
 }
-__device__ __forceinline__ bool hub_search(const Ctx& C, uint32_t o, uint32_t e, uint32_t v, uint32_t tree = kNone) {
+__device__ __forceinline__ bool hub_search(const Ctx& C, uint32_t o, uint32_t e, uint32_t v) {
     uint32_t l = o, r = e;
-    if (tree != kNone) {
-        l = tree_lower_bound(C, C.sh->hub_keys + tree, o, e, v);
-    } else {
-        while (l < r) {
-            const uint32_t mid = (l + r) >> 1;
-            if (C.N(mid) < v) l = mid + 1;
-            else r = mid;
-        }
+    while (l < r) {
+        const uint32_t mid = (l + r) >> 1;
+        if (C.N(mid) < v) l = mid + 1;
+        else r = mid;
     }
     return l < e && C.N(l) == v;
 }
+__device__ __forceinline__ bool hub_search_tree(const Ctx& C, uint32_t o, uint32_t e, uint32_t v, uint32_t tree) {
+    if (tree == kNone) return hub_search(C, o, e, v);
+    const uint32_t l = tree_lower_bound(C, C.sh->hub_keys + tree, o, e, v);
+    return l < e && C.N(l) == v;
+}
 // dependent loads of one search in a row of deg entries: log2(deg), or with a
-// search tree one node per 3 bits above the 32-entry block plus the block
+// search tree one node per 3 bits above the 32-entry block, plus the block
 __device__ __forceinline__ uint32_t search_cost(uint32_t deg, bool trees) {
     const uint32_t bits = 32u - __clz(deg);
     return trees && hub_has_tree(deg) ? (bits + 4u) / 3u : bits;
 }
 // factor in quarters: deg > (factor / 4) |L| cost(deg)
-__device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list, uint32_t factor, bool trees) {
+__device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list, uint32_t factor, bool trees = false) {
     return ADSB_HUB_PROBE && list && factor &&
            4ull * deg > static_cast<unsigned long long>(factor) * list * search_cost(deg, trees);
 }
@@ -609,7 +598,10 @@ __device__ __forceinline__ void hub_phase(Ctx& C, Store& S, Shared& sh, uint32_t
         const uint32_t h = pi / L, j = pi - h * L;
         const uint32_t q = l_lo + j;
         const uint32_t v = S.qv[l_t ? S.tpos(q) : q];
-        if (hub_search(C, sh.hub_o[h], sh.hub_e[h], v, sh.hub_tree[h])) body(sh.hub_slot[h], sh.hub_val[h], v, kNoTok);
+        bool hit;
+        if constexpr (Store::kTrees) hit = hub_search_tree(C, sh.hub_o[h], sh.hub_e[h], v, sh.hub_tree[h]);
+        else hit = hub_search(C, sh.hub_o[h], sh.hub_e[h], v);
+        if (hit) body(sh.hub_slot[h], sh.hub_val[h], v, kNoTok);
     }
 }
 
@@ -720,19 +712,20 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             slot = S.find(u, meta);
             val = prep(slot, meta, e - o);
             scanned = e - o;
-            if (is_hub(e - o, l_hi - l_lo, C.hub_factor, sh.hub_ref != nullptr)) {
+            const bool trees = Store::kTrees && sh.hub_ref != nullptr;
+            if (is_hub(e - o, l_hi - l_lo, C.hub_factor, trees)) {
                 const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
                 if (h < kMaxHubs) {
                     sh.hub_o[h] = o;
                     sh.hub_e[h] = e;
                     sh.hub_slot[h] = slot;
                     sh.hub_val[h] = val;
-                    sh.hub_tree[h] = sh.hub_ref != nullptr && hub_has_tree(e - o) ? __ldg(sh.hub_ref + u) : kNone;
+                    if constexpr (Store::kTrees)
+                        sh.hub_tree[h] = trees && hub_has_tree(e - o) ? __ldg(sh.hub_ref + u) : kNone;
                     nv = 0;
-                    scanned = (l_hi - l_lo) * search_cost(e - o, sh.hub_ref != nullptr);  // searches, not scans
+                    scanned = (l_hi - l_lo) * search_cost(e - o, trees);  // searches, not scans
                 }
             }
-            if (nv != 0 && C.bulk_min != 0 && e - o >= C.bulk_min) bulk_prefetch_row(C, o, e);
         }
         const uint32_t wdeg = __reduce_add_sync(kFull, scanned);
         if (C.lane == 0 && wdeg) counter[C.warp] += wdeg;
@@ -809,19 +802,20 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             uint32_t meta;
             slot = S.find(u, meta);
             val = prep(slot, meta, deg);
-            if (is_hub(deg, l_hi - l_lo, C.hub_factor, sh.hub_ref != nullptr)) {
+            const bool trees = Store::kTrees && sh.hub_ref != nullptr;
+            if (is_hub(deg, l_hi - l_lo, C.hub_factor, trees)) {
                 const uint32_t h = atomicAdd(&sh.n_hub[par], 1u);
                 if (h < kMaxHubs) {
                     sh.hub_o[h] = o;
                     sh.hub_e[h] = o + deg;
                     sh.hub_slot[h] = slot;
                     sh.hub_val[h] = val;
-                    sh.hub_tree[h] = sh.hub_ref != nullptr && hub_has_tree(deg) ? __ldg(sh.hub_ref + u) : kNone;
-                    hub_reads = (l_hi - l_lo) * search_cost(deg, sh.hub_ref != nullptr);
+                    if constexpr (Store::kTrees)
+                        sh.hub_tree[h] = trees && hub_has_tree(deg) ? __ldg(sh.hub_ref + u) : kNone;
+                    hub_reads = (l_hi - l_lo) * search_cost(deg, trees);
                     deg = 0;
                 }
             }
-            if (deg != 0 && C.bulk_min != 0 && deg >= C.bulk_min) bulk_prefetch_row(C, o, o + deg);
         }
         {
             const uint32_t wr = __reduce_add_sync(kFull, hub_reads);
@@ -1004,17 +998,10 @@ struct Meet {
 // Loop state of bfs() between levels: what a sample carries from the
 // shared-memory table to a global region when the table fills up at a claim
 // pass (the completed levels are copied; that level's claims are redone).
-// mode (set by the caller before bfs() resumes): 1 = resume at the claim pass
-// of the current level on another store (its probe already ran); 2 = resume at
-// the top of the level loop on the same store (after a join level).
-// clean: bfs() left before the claim pass ran (predicted overflow), so the
-// table holds completed levels only.
 struct BfsState {
     uint32_t s_lo, s_hi, t_lo, t_hi, a, b, used;
     unsigned long long deg_s, deg_t;
-    uint32_t mode, clean;
 };
-constexpr uint32_t kResumeClaim = 1, kResumeTop = 2;
 
 #ifndef ADSB_MIGRATE
 #define ADSB_MIGRATE 1
@@ -1023,11 +1010,10 @@ constexpr uint32_t kResumeClaim = 1, kResumeTop = 2;
 template <class Store>
 __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nullptr) {
     Shared& sh = *C.sh;
-    // io != nullptr on entry with io->mode set: resume a migrated sample at
-    // the claim pass of its current level (the probe found no meeting there),
-    // or a joined sample at the top of the loop; on a claim-pass overflow of
-    // the table (observed or predicted) the state is written to io.
-    const bool resume = io != nullptr && io->mode != 0;
+    // io != nullptr on entry with io->used == ~0u: resume a migrated sample at
+    // the claim pass of its current level (the probe found no meeting there);
+    // on a claim-pass overflow of the table the state is written to io.
+    const bool resume = io != nullptr && io->used == ~0u;
     // Level L = a + b uses counter slot L % 3; thread 0 zeroes slot (L+1) % 3
     // as level L starts: every thread read that slot (as level L-2's) before
     // level L-1's barriers, and level L+1 writes it only after level L's.
@@ -1065,20 +1051,13 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
     unsigned long long deg_t = by_count ? 1ull : C.O(t + 1) - C.O(t);
     bool skip_next = false;
     if (resume) {
-        s_lo = io->s_lo, s_hi = io->s_hi, t_lo = io->t_lo, t_hi = io->t_hi, a = io->a, b = io->b;
-        used = io->mode == kResumeTop ? io->used : 0u;
+        s_lo = io->s_lo, s_hi = io->s_hi, t_lo = io->t_lo, t_hi = io->t_hi, a = io->a, b = io->b, used = 0;
         deg_s = io->deg_s, deg_t = io->deg_t;
-        skip_next = io->mode == kResumeClaim;
+        skip_next = true;
     }
-    auto migrate = [&](uint32_t used_now, uint32_t clean) -> Meet {
-        if (io) *io = BfsState{s_lo, s_hi, t_lo, t_hi, a, b, used_now, deg_s, deg_t, 0u, clean};
+    auto migrate = [&](uint32_t used_now) -> Meet {
+        if (io) *io = BfsState{s_lo, s_hi, t_lo, t_hi, a, b, used_now, deg_s, deg_t};
         return {a, b, io ? 3 : 1};
-    };
-    // A claim pass whose adjacency is several times the table's room will
-    // overflow it: leave before it runs, and the caller tries a join level.
-    auto predicted = [&](unsigned long long deg) {
-        return io != nullptr && C.join_factor != 0 &&
-               deg > static_cast<unsigned long long>(C.join_factor) * S.join_room(used);
     };
     for (;;) {
         const bool skip_probe = skip_next;  // first level of a resumed sample: its probe already ran
@@ -1193,7 +1172,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                       },
                       t_lo, t_hi, true);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
-            if (predicted(deg_s)) return migrate(used, 1u);
             }
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
@@ -1215,7 +1193,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
             __syncthreads();  // counters and overflow final before any thread reads them
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
-            if (sh.overflow) return migrate(used, 0u);
+            if (sh.overflow) return migrate(used);
             if (!S.pre_zeroed())
             for_edges(C, S, s_lo, s_hi, false, sh.st_edges,
                       [&](uint32_t slot, uint32_t, uint32_t) { return S.sigma(slot); },
@@ -1248,7 +1226,6 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                       },
                       s_lo, s_hi, false);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
-            if (predicted(deg_t)) return migrate(used, 1u);
             }
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
@@ -1267,7 +1244,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
             __syncthreads();
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.t_cnt = min(t_hi + added, S.qcap);
-            if (sh.overflow) return migrate(used, 0u);
+            if (sh.overflow) return migrate(used);
             t_lo = t_hi;
             t_hi += added;
             used += sh.lvl_ins[cur];
@@ -1416,7 +1393,9 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
     __syncthreads();
     uint32_t probes = 0;
     // cur's search tree (hub_index.cuh), when it has one
-    const uint32_t tree = sh.hub_ref != nullptr && hub_has_tree(end - beg) ? __ldg(sh.hub_ref + cur) : kNone;
+    uint32_t tree = kNone;
+    if constexpr (Store::kTrees)
+        if (sh.hub_ref != nullptr && hub_has_tree(end - beg)) tree = __ldg(sh.hub_ref + cur);
 #if ADSB_KARY
     if (hi - lo <= 2 * (kBT / 32)) {
         // short list: one warp per entry, 32-ary search (each round one
@@ -1464,7 +1443,7 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
         const uint32_t sl = S.find(q, m);
         if (sl == kNone || m_is_t(m) != want_t || m_dist(m) != want_dist || (want_t && !(m & kMetaDag))) continue;
         uint32_t l = beg, h = end;
-        if (tree != kNone) {
+        if (Store::kTrees && tree != kNone) {
             l = tree_lower_bound(C, sh.hub_keys + tree, beg, end, q);
             probes += search_cost(end - beg, true);
         } else {
@@ -1628,14 +1607,12 @@ __device__ bool backtrack(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& 
             const uint32_t lo = want_t ? S.tlev[want_dist] : S.slev[want_dist];
             const uint32_t hi = want_t ? S.tlev[want_dist + 1] : S.slev[want_dist + 1];
             const uint32_t deg = end - beg;
-            if (hi - lo <= 4 * kBT && 2ull * (hi - lo) * search_cost(deg, sh.hub_ref != nullptr) < deg)
+            if (hi - lo <= 4 * kBT && 2ull * (hi - lo) * search_cost(deg, Store::kTrees && sh.hub_ref != nullptr) < deg)
                 found = level_pick(C, S, beg, end, lo, hi, want_t, want_dist, r, cur, cmeta, csig);
         }
 #endif
         // the next round's neighbour id is loaded one round ahead, so its
         // latency overlaps this round's barriers (hub steps take many rounds)
-        if (!found && C.tid == 0 && C.bulk_min != 0 && end - beg >= max(C.bulk_min, 2u * kBT))
-            bulk_prefetch_row(C, beg, end);
         uint32_t q_next = !found && beg + C.tid < end ? C.N(beg + C.tid) : 0u;
         for (uint32_t base = beg; !found && base < end; base += kBT) {
             const uint32_t i = base + C.tid;
@@ -1764,7 +1741,7 @@ template <int kMode, class Store>
 __device__ int run_sample(Ctx& C, Store& S, const SamplerParams& p, SplitMix64& rng, uint32_t s, uint32_t t,
                           uint32_t frame_local, BfsState* io = nullptr) {
     Shared& sh = *C.sh;
-    if (!(io && io->mode == kResumeTop)) S.begin(C.tid);  // a joined sample continues on its table
+    S.begin(C.tid);
     if (C.tid == 0) {
         sh.overflow = 0;
     }
@@ -1833,10 +1810,10 @@ __device__ __forceinline__ SmemStoreT<kVec> make_smem_store(const SamplerParams&
     return sm;
 }
 
-template <bool kGlobalOnly>
-__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly> make_global_store(const SamplerParams& p, uint32_t slot,
-                                                                           uint32_t tag) {
-    GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly> gs;
+template <bool kGlobalOnly, bool kTrees = false>
+__device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly, kTrees> make_global_store(const SamplerParams& p,
+                                                                                                uint32_t slot, uint32_t tag) {
+    GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly, kTrees> gs;
     gs.st = p.state + 2ull * p.slot_stride * slot;
     gs.qv = p.queue + static_cast<size_t>(p.slot_stride) * slot;
     gs.tlev = p.tlev + static_cast<size_t>(p.level_cap) * slot;
@@ -1891,7 +1868,6 @@ __device__ void release_region(const SamplerParams& p, uint32_t region, uint32_t
 // exactly the state the global store would have built.
 template <bool kVec, class GS>
 __device__ void migrate_to_global(Ctx& C, const SamplerParams& p, GS& gs, const BfsState& st) {
-    // (entries beyond the completed levels, e.g. a failed join's claims, are skipped like the failed level's)
     Shared& sh = *C.sh;
     auto sm = make_smem_store<kVec>(p, sh);
     const unsigned long long hi_word = gs.clear ? GS::kPresent : static_cast<unsigned long long>(gs.tag) << 32;
@@ -1915,127 +1891,6 @@ __device__ void migrate_to_global(Ctx& C, const SamplerParams& p, GS& gs, const 
     __syncthreads();
 }
 
-#ifndef ADSB_JOIN
-#define ADSB_JOIN 1
-#endif
-// Put the completed levels of a migrated sample back into the (cleared)
-// shared-memory table: the queue still lists their vertices, the region holds
-// side, distance and sigma (migrate_to_global wrote them).
-template <bool kVec, class GS>
-__device__ void rebuild_table(Ctx& C, SmemStoreT<kVec>& sm, GS& gs, const BfsState& st) {
-    for (uint32_t i = C.tid; i < st.s_hi + st.t_hi; i += kBT) {
-        const uint32_t v = sm.qv[i < st.s_hi ? i : sm.tpos(i - st.s_hi)];
-        const uint32_t meta = static_cast<uint32_t>(__ldcg(gs.st + 2ull * v));
-        const unsigned long long sg = __ldcg(gs.st + 2ull * v + 1);
-        bool ins;
-        uint32_t m;
-        const uint32_t slot = sm.template claim<false>(v, meta, ins, m);
-        sm.sig[slot] = sg;  // each vertex is listed once
-        if (meta & kMetaDag) sm.set_dag(slot);
-    }
-    __syncthreads();
-}
-
-// Join level. A sample reaches this point when level L+1 of side X (frontier
-// F = X's level L; the other side's frontier is G) would not fit the table,
-// after the probe found no edge between F and G, i.e. dist(s, t) >= a + b + 2.
-// Claiming all of N(F) would move the sample to a global region: tens of
-// thousands of random 16-byte claims for a level of which only the vertices
-// adjacent to G can ever lie on a shortest path of length a + b + 2. So the
-// level is JOINED instead of claimed:
-//   1. mark N(F) in the region's vertex bitmap (fire-and-forget atomics on
-//      n / 8 bytes instead of 16 n);
-//   2. scan N(G): every marked, unvisited vertex x is claimed in the table as
-//      level L+1 of side X -- the set J = N(F) & N(G) \ visited;
-//   3. unmark N(F);
-//   4. (s side) sigma(x) = sum of sigma(u) over u in F adjacent to x.
-// If J is empty (the distance is larger) or does not fit, the sample takes the
-// global region as before. Otherwise J stands in for level L+1: it holds every
-// vertex of that level adjacent to G, so the next probe meets at distance
-// a + b + 2 with exactly the meeting edges, DAG flags, sigma sums and level
-// lists (restricted to shortest-path vertices) of the full level: rebuild and
-// backtrack read nothing else of it. Returns true with `st` advanced by the
-// joined level (resume with kResumeTop).
-template <bool kVec>
-__device__ bool join_level(Ctx& C, SmemStoreT<kVec>& sm, uint32_t* bits, BfsState& st) {
-    Shared& sh = *C.sh;
-    ADSB_JOIN_COUNT(0);
-    const bool side_t = st.deg_s > st.deg_t;  // the side bfs() was expanding
-    const uint32_t f_lo = side_t ? st.t_lo : st.s_lo, f_hi = side_t ? st.t_hi : st.s_hi;
-    const uint32_t g_lo = side_t ? st.s_lo : st.t_lo, g_hi = side_t ? st.s_hi : st.t_hi;
-    const uint32_t used = st.s_hi + st.t_hi;
-    if (C.tid == 0) {
-        sh.lvl_cnt[0] = sh.lvl_ins[0] = sh.lvl_deg[0] = 0;
-        sh.overflow = 0;
-        sh.st_verts += 3 * (f_hi - f_lo) + (g_hi - g_lo);
-    }
-    sm.set_level(&sh.lvl_ins[0], used);
-    __syncthreads();
-    auto no_payload = [](uint32_t, uint32_t, uint32_t) { return 0ull; };
-    for_edges(C, sm, f_lo, f_hi, side_t, sh.st_edges, no_payload,
-              [&](uint32_t, unsigned long long, uint32_t v) { atomicOr(bits + (v >> 5), 1u << (v & 31)); });
-    const uint32_t new_meta = side_t ? (kMetaT | (st.b + 1)) : st.a + 1;
-    for_edges(C, sm, g_lo, g_hi, !side_t, sh.st_edges, no_payload,
-              [&](uint32_t, unsigned long long, uint32_t v) {
-                  if (!((__ldcg(bits + (v >> 5)) >> (v & 31)) & 1u)) return;
-                  bool ins;
-                  uint32_t m;
-                  sm.claim(v, new_meta, ins, m);
-                  if (!ins) return;
-                  const uint32_t k = aggregated_inc(&sh.lvl_cnt[0]);
-                  if (side_t) {
-                      if (sm.queue_ok(st.s_hi, st.t_hi + k + 1)) sm.qv[sm.tpos(st.t_hi + k)] = v;
-                      else sh.overflow = 1;
-                  } else {
-                      if (sm.queue_ok(st.s_hi + k + 1, st.t_hi)) sm.qv[st.s_hi + k] = v;
-                      else sh.overflow = 1;
-                  }
-              });
-    for_edges(C, sm, f_lo, f_hi, side_t, sh.st_edges, no_payload,
-              [&](uint32_t, unsigned long long, uint32_t v) { __stcg(bits + (v >> 5), 0u); });
-    const uint32_t added = sh.lvl_cnt[0];  // for_edges ended with a barrier
-    const bool level_ok = side_t ? st.b + 3 <= sm.level_cap : st.a + 3 <= sm.level_cap;
-    if (sh.overflow || added == 0 || !level_ok) {
-        ADSB_JOIN_COUNT(added == 0 ? 2 : 3);
-        __syncthreads();
-        return false;
-    }
-    ADSB_JOIN_COUNT(1);
-    if (!side_t) {
-        // frontier hubs are searched for the (few) joined vertices instead of scanned
-        for_edges(C, sm, f_lo, f_hi, false, sh.st_edges,
-                  [&](uint32_t slot, uint32_t, uint32_t) { return sm.sigma(slot); },
-                  [&](uint32_t, unsigned long long su, uint32_t v) {
-                      uint32_t m;
-                      const uint32_t sl = sm.find(v, m);
-                      if (sl != kNone && !m_is_t(m) && m_dist(m) == st.a + 1) sm.add_sigma(sl, su);
-                  },
-                  st.s_hi, st.s_hi + added, false);
-    }
-    if (side_t) {
-        st.t_lo = st.t_hi;
-        st.t_hi += added;
-        st.b += 1;
-        if (C.tid == 0) {
-            sh.t_cnt = st.t_hi;
-            sm.tlev[st.b + 1] = st.t_hi;
-        }
-        st.deg_t = level_degrees(C, sm, st.t_lo, st.t_hi, true, 0);
-    } else {
-        st.s_lo = st.s_hi;
-        st.s_hi += added;
-        st.a += 1;
-        if (C.tid == 0) {
-            sh.s_cnt = st.s_hi;
-            sm.slev[st.a + 1] = st.s_hi;
-        }
-        st.deg_s = level_degrees(C, sm, st.s_lo, st.s_hi, false, 0);
-    }
-    st.used = used + added;
-    st.mode = kResumeTop;
-    return true;
-}
-
 // gtag: the global-only kernel's generation tag for its own region (block-uniform).
 template <int kMode, bool kGlobalOnly, bool kVec>
 __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint32_t frame_local, uint32_t& gtag) {
@@ -2047,6 +1902,7 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
     ADSB_PHASE_MARK(os0);
     int rc = 1;
     BfsState mig{};
+    mig.used = 0;
     if constexpr (!kGlobalOnly) {
         if (p.use_smem) {
             auto sm = make_smem_store<kVec>(p, *C.sh);
@@ -2059,14 +1915,14 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
     }
     const bool fell_back = rc == 1 || rc == 3;
     (void)fell_back;
-    // attempt 1 only after a joined sample ran out of table levels (rc 1): from scratch on a region
-    for (int attempt = 0; attempt < 2 && (rc == 1 || rc == 3); ++attempt) {
+    if (rc == 1 || rc == 3) {
         uint32_t region = blockIdx.x, tag;
         if constexpr (kGlobalOnly) {
             tag = ++gtag;
         } else {
             Shared& sh = *C.sh;
             if (C.tid == 0) {
+                sh.n_fallbacks += 1;
                 sh.g_region = acquire_region(p);
                 sh.g_tag = __ldcg(p.slot_tag + sh.g_region) + 1u;
             }
@@ -2085,43 +1941,9 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
             tag = 1;
             if constexpr (kGlobalOnly) gtag = 1;
         }
-        auto gs = make_global_store<kGlobalOnly>(p, region, tag);
+        auto gs = make_global_store<kGlobalOnly, kVec>(p, region, tag);
         if constexpr (!kGlobalOnly) {
-            if (rc == 3) {
-                bool joined = false;
-                if (ADSB_JOIN && p.join_bits != nullptr && !gs.clear) {
-                    auto sm = make_smem_store<kVec>(p, *C.sh);
-                    if (!mig.clean) {
-                        // the failed claim pass left part of its level in the table
-                        migrate_to_global<kVec>(C, p, gs, mig);
-                        rebuild_table<kVec>(C, sm, gs, mig);
-                    }
-                    joined = join_level<kVec>(C, sm, p.join_bits + static_cast<size_t>(p.join_words) * region, mig);
-                    if (joined) {
-                        __syncthreads();  // the bitmap is clear and nobody reads the region any more
-                        if (C.tid == 0) release_region(p, region, tag);
-                        rc = run_sample<kMode>(C, sm, p, rng, s, t, frame_local, &mig);
-                        mig.mode = 0;
-                        if (rc == 3) {
-                            // cannot happen (the level after a join always meets); a joined
-                            // level is partial, so such a sample would restart from scratch
-                            sm.clear_all(C.tid);
-                            __syncthreads();
-                            rc = 1;
-                        }
-                        continue;  // done unless rc == 1
-                    }
-                    if (mig.clean) {
-                        migrate_to_global<kVec>(C, p, gs, mig);
-                    } else {
-                        sm.clear_all(C.tid);
-                        __syncthreads();
-                    }
-                } else {
-                    migrate_to_global<kVec>(C, p, gs, mig);
-                }
-            }
-            if (C.tid == 0) C.sh->n_fallbacks += 1;
+            if (rc == 3) migrate_to_global<kVec>(C, p, gs, mig);
         }
 #if ADSB_FALLBACK_FILTER
         // the table is empty here (the overflowed attempt cleared it, or the
@@ -2139,7 +1961,7 @@ __device__ void one_sample(Ctx& C, const SamplerParams& p, SplitMix64& rng, uint
                 }
             }
 #endif
-        if (rc == 3) mig.mode = kResumeClaim;
+        if (rc == 3) mig.used = ~0u;  // resume at the claim pass
         rc = run_sample<kMode>(C, gs, p, rng, s, t, frame_local, rc == 3 ? &mig : nullptr);
         if constexpr (!kGlobalOnly) {
             __syncthreads();  // every thread is done with the region
@@ -2270,9 +2092,6 @@ __global__ void __launch_bounds__(kBT, kGlobalOnly ? ADSB_GLOBAL_MINB * 256 / kB
 #endif
     C.tid = threadIdx.x;
     C.hub_factor = p.hub_factor;
-    C.join_factor = (ADSB_JOIN && !kGlobalOnly && p.join_bits != nullptr && p.clear_layout == 0) ? p.join_factor : 0u;
-    C.bulk_min = p.bulk_min;
-    C.nnz = p.nnz;
     C.lane = threadIdx.x & 31;
     C.warp = threadIdx.x >> 5;
     C.sh = &sh;

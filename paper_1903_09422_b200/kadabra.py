@@ -142,13 +142,6 @@ def sample_frames(g: Graph, seed: int, samples_per_frame: int, first: int, count
     return [incs[int(offsets[i]):int(offsets[i + 1])].copy() for i in range(count)]
 
 
-def sampler_counters(device: int = 0, reset: bool = True) -> dict[str, int]:
-    """Diagnostic counters of the block sampler's join levels (adsb_sampler_counters)."""
-    out = np.zeros(4, dtype=np.uint64)
-    check(lib().adsb_sampler_counters(device, out.ctypes.data_as(u64p), 1 if reset else 0))
-    return dict(zip(("attempts", "joined", "empty", "too_large"), (int(x) for x in out)))
-
-
 def exact_bc(g: Graph, device: int = -1) -> tuple[np.ndarray, float]:
     """Exact betweenness of every vertex on the device (Brandes, f64), normalised by
     n(n-1) like BcResult::scores; the validation the reference runs with ApspOracle
@@ -161,4 +154,4 @@ def exact_bc(g: Graph, device: int = -1) -> tuple[np.ndarray, float]:
 
 
 __all__ = ["allocate_deltas", "compute_omega", "f_bound", "g_bound", "kadabra_check", "StopReason",
-           "to_string", "BcResult", "estimate_bc", "exact_bc", "sample_frames", "sampler_counters", "Variant"]
+           "to_string", "BcResult", "estimate_bc", "exact_bc", "sample_frames", "Variant"]
