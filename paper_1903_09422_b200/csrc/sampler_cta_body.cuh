@@ -8,6 +8,12 @@ constexpr uint32_t kMaxHubs = 32;
 #ifndef ADSB_HUB_PROBE
 #define ADSB_HUB_PROBE 1
 #endif
+#ifndef ADSB_VEC_FALLBACK
+#define ADSB_VEC_FALLBACK 1  // vector kernels: fallback samples read adjacency as 16-byte vectors too
+#endif
+#ifndef ADSB_CLAIM_PREFETCH
+#define ADSB_CLAIM_PREFETCH 1  // ... and prefetch a vector's four state words in claim passes
+#endif
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
 constexpr uint32_t kMetaT = 1u << 31;
@@ -265,6 +271,8 @@ struct SmemStoreT {
     __device__ bool room_for(unsigned long long edges) const {
         return ins_base < limit && edges <= limit - ins_base;
     }
+    // insertions the table still takes after `used`
+    __device__ uint32_t table_room(uint32_t used) const { return used < limit ? limit - used : 0u; }
 };
 using SmemStore = SmemStoreT<false>;
 
@@ -311,11 +319,30 @@ using SmemStore = SmemStoreT<false>;
 #ifndef ADSB_LOWDEG_COUNT
 #define ADSB_LOWDEG_COUNT 1
 #endif
+// 16-byte compare-and-swap on a (meta, sigma) state entry (ATOMG.E.CAS.128).
+__device__ __forceinline__ ulonglong2 cas128(unsigned long long* p, ulonglong2 cmp, ulonglong2 val) {
+    ulonglong2 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, n, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 n, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, n;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old.x), "=l"(old.y)
+        : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+        : "memory");
+    return old;
+}
+__device__ __forceinline__ ulonglong2 ldcg2(const unsigned long long* p) {
+    return __ldcg(reinterpret_cast<const ulonglong2*>(p));
+}
 template <uint32_t kU, bool kBatch = false, bool kTr = false>
 struct GlobalStoreT {
     static constexpr uint32_t kLoadBatch = kU;
-    static constexpr bool kVec4 = false;
-    static constexpr bool kTrees = kTr;  // fallback samples of the vector kernels
+    // fallback samples of the vector kernels: 16-byte adjacency reads and hub search trees too
+    static constexpr bool kVec4 = kTr && ADSB_VEC_FALLBACK;
+    static constexpr bool kTrees = kTr;
+    uint32_t* crange;  // vectorised reads: row ranges of the chunk (the dynamic shared memory's tail)
     static constexpr bool kBatchClaims = kBatch;  // global-store-only kernels
     static constexpr bool kSlotIsVertex = true;   // find() returns the vertex as its slot
     static constexpr uint32_t kMaxDist = kMetaDist - 1;
@@ -391,11 +418,14 @@ struct GlobalStoreT {
             if (inserted) fset(v);
             return v;
         }
-        unsigned long long x = __ldcg(st + 2ull * v);
-        if (static_cast<uint32_t>(x >> 32) != tag) {
+        // tagged: one 16-byte load, then one 16-byte CAS that stamps the word and
+        // zeroes sigma together, so adders that see the stamp never race with
+        // an initialisation (a losing CAS returns the winner's stamped entry)
+        ulonglong2 x = ldcg2(st + 2ull * v);
+        while (static_cast<uint32_t>(x.x >> 32) != tag) {
             const unsigned long long want = (static_cast<unsigned long long>(tag) << 32) | new_meta;
-            const unsigned long long prev = atomicCAS(st + 2ull * v, x, want);
-            if (prev == x) {
+            const ulonglong2 prev = cas128(st + 2ull * v, x, make_ulonglong2(want, 0ull));
+            if (prev.x == x.x && prev.y == x.y) {
                 inserted = true;
                 meta = new_meta;
                 fset(v);
@@ -403,7 +433,7 @@ struct GlobalStoreT {
             }
             x = prev;
         }
-        meta = static_cast<uint32_t>(x);
+        meta = static_cast<uint32_t>(x.x);
         return v;
     }
     // Batched low-degree claims: the CAS is issued early (claim_issue) and
@@ -421,12 +451,14 @@ struct GlobalStoreT {
         if (inserted) fset(v);
         return v;
     }
-    // sigma is zero before the claim, so claims and sums share one pass
-    __device__ bool pre_zeroed() const { return clear; }
+    // Claims and sigma sums share one pass when sigma is zero at the claim: the
+    // cleared layout, and the tagged layout of a fallback sample (the 16-byte
+    // claim zeroes it). Global-only tagged kernels keep the second pass: their
+    // one-pass levels claim speculatively on the meeting level, the biggest,
+    // whose sums the second pass skips.
+    __device__ bool pre_zeroed() const { return clear || filt != nullptr; }
     static constexpr bool kSpeculativeClaims = true;  // no capacity limit: probe and claim in one pass
-    __device__ void zero_sigma(uint32_t slot) {
-        if (!clear) st[2ull * slot + 1] = 0ull;
-    }
+    __device__ void zero_sigma(uint32_t) {}  // every claim leaves sigma zero
     __device__ void add_sigma(uint32_t slot, unsigned long long x) { atomicAdd(st + 2ull * slot + 1, x); }
     __device__ void set_dag(uint32_t slot) { atomicOr(st + 2ull * slot, static_cast<unsigned long long>(kMetaDag)); }
     __device__ void prefetch(uint32_t v) const { asm volatile("prefetch.global.L2 [%0];" ::"l"(st + 2ull * v)); }
@@ -439,6 +471,7 @@ struct GlobalStoreT {
     __device__ uint32_t tpos(uint32_t j) const { return qcap - 1 - j; }
     __device__ bool room_for(unsigned long long) const { return filt == nullptr; }
     __device__ void set_level(uint32_t*, uint32_t) {}
+    __device__ uint32_t table_room(uint32_t) const { return 0xFFFFFFFFu; }  // no capacity limit
 };
 
 // CSR reads carry an L2 eviction-priority hint: evict_last when the CSR fits
@@ -608,7 +641,7 @@ __device__ __forceinline__ void hub_phase(Ctx& C, Store& S, Shared& sh, uint32_t
 template <class Store, class Prep, class Issue, class Body>
 __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list, unsigned long long* counter,
                               Prep prep, Issue issue, Body body, uint32_t l_lo = 0, uint32_t l_hi = 0,
-                              bool l_t = false) {
+                              bool l_t = false, bool touch_all = false) {
     Shared& sh = *C.sh;
     ADSB_PHASE_ADD(6, 1);
     if (C.low_degree) {
@@ -768,6 +801,17 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
             if (j + ADSB_PF_DIST * kBT < o_end)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const uint4*>(C.nbrs) + g + ADSB_PF_DIST * kBT));
             const uint32_t e0 = g * 4u;
+            // touch_all (claim passes on a global region): every entry's state
+            // word is read, so the vector's four go to L2 together before the
+            // first is used instead of one dependent HBM round trip each
+            if constexpr (Store::kSlotIsVertex && ADSB_CLAIM_PREFETCH) {
+                if (touch_all) {
+                    if (e0 >= r_lo && e0 < r_hi) S.prefetch(x.x);
+                    if (e0 + 1 >= r_lo && e0 + 1 < r_hi) S.prefetch(x.y);
+                    if (e0 + 2 >= r_lo && e0 + 2 < r_hi) S.prefetch(x.z);
+                    if (e0 + 3 >= r_lo && e0 + 3 < r_hi) S.prefetch(x.w);
+                }
+            }
 #pragma unroll 1
             for (uint32_t k = 0; k < 4; ++k) {
                 const uint32_t idx = e0 + k;
@@ -932,10 +976,10 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
 template <class Store, class Prep, class Body>
 __device__ __forceinline__ void for_edges(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t_list,
                                           unsigned long long* counter, Prep prep, Body body, uint32_t l_lo = 0,
-                                          uint32_t l_hi = 0, bool l_t = false) {
+                                          uint32_t l_hi = 0, bool l_t = false, bool touch_all = false) {
     for_edges_tok(C, S, lo, hi, t_list, counter, prep, [](uint32_t) { return kNoTok; },
                   [&](uint32_t su, unsigned long long val, uint32_t v, unsigned long long) { body(su, val, v); },
-                  l_lo, l_hi, l_t);
+                  l_lo, l_hi, l_t, touch_all);
 }
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long x, int src) {
@@ -1006,6 +1050,9 @@ struct BfsState {
 #ifndef ADSB_MIGRATE
 #define ADSB_MIGRATE 1
 #endif
+#ifndef ADSB_PREDICT_FACTOR
+#define ADSB_PREDICT_FACTOR 2  // migrate before a claim pass over more than this x the table's room (0: never)
+#endif
 
 template <class Store>
 __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nullptr) {
@@ -1058,6 +1105,15 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
     auto migrate = [&](uint32_t used_now) -> Meet {
         if (io) *io = BfsState{s_lo, s_hi, t_lo, t_hi, a, b, used_now, deg_s, deg_t};
         return {a, b, io ? 3 : 1};
+    };
+    // A claim pass over several times more adjacency than the table has room
+    // left fills it: migrate before the pass instead of after (the level's
+    // claims run once, on the region). A wrong guess only costs the sample the
+    // slower store. Only the table has a capacity (join_room), and only a
+    // sample that can migrate (io) and is not already resumed takes this exit.
+    auto predicted = [&](unsigned long long deg) {
+        return ADSB_PREDICT_FACTOR != 0 && io != nullptr && !resume &&
+               deg > static_cast<unsigned long long>(ADSB_PREDICT_FACTOR) * S.table_room(used);
     };
     for (;;) {
         const bool skip_probe = skip_next;  // first level of a resumed sample: its probe already ran
@@ -1172,6 +1228,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                       },
                       t_lo, t_hi, true);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
+            if (predicted(deg_s)) return migrate(used);
             }
             // ---- no meeting: claim level a+1, then accumulate its sigma
             const uint32_t meta_new = a + 1;
@@ -1189,7 +1246,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                               if (S.queue_ok(pos + 1, t_hi)) S.qv[pos] = v;
                               else sh.overflow = 1;
                           }
-                      });
+                      },
+                      0, 0, false, true);
             __syncthreads();  // counters and overflow final before any thread reads them
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.s_cnt = min(s_hi + added, S.qcap);
@@ -1226,6 +1284,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                       },
                       s_lo, s_hi, false);
             if (sh.lvl_met[cur]) return {a, b, 0};  // for_edges ended with a barrier
+            if (predicted(deg_t)) return migrate(used);
             }
             const uint32_t meta_new = kMetaT | (b + 1);
             for_edges(C, S, t_lo, t_hi, true, sh.st_edges,
@@ -1240,7 +1299,8 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
                               if (S.queue_ok(s_hi, j + 1)) S.qv[S.tpos(j)] = v;
                               else sh.overflow = 1;
                           }
-                      });
+                      },
+                      0, 0, false, true);
             __syncthreads();
             const uint32_t added = sh.lvl_cnt[cur];
             if (C.tid == 0) sh.t_cnt = min(t_hi + added, S.qcap);
@@ -1821,6 +1881,15 @@ __device__ __forceinline__ GlobalStoreT<ADSB_LOAD_BATCH, kGlobalOnly, kTrees> ma
     gs.dq = p.dagq + static_cast<size_t>(p.slot_stride) * slot;
     gs.clear = p.clear_layout != 0;
     gs.filt = nullptr;
+    {
+        // the vector kernels' row ranges sit behind the table and queue (make_smem_store)
+        const uint32_t H = p.hash_cap;
+        uint32_t* tail = reinterpret_cast<uint32_t*>(adsb_dyn + H) + H + H / 2;
+#if ADSB_SMEM_FILTER
+        tail += SmemStoreT<kTrees>::kFbWords;
+#endif
+        gs.crange = kTrees ? tail : nullptr;
+    }
     gs.tag = tag;
     gs.qcap = p.n;
     gs.level_cap = p.level_cap;
