@@ -8,6 +8,9 @@ constexpr uint32_t kMaxHubs = 32;
 #ifndef ADSB_HUB_PROBE
 #define ADSB_HUB_PROBE 1
 #endif
+#ifndef ADSB_PROBE_PREFETCH
+#define ADSB_PROBE_PREFETCH 1
+#endif
 #ifndef ADSB_VEC_FALLBACK
 #define ADSB_VEC_FALLBACK 1  // vector kernels: fallback samples read adjacency as 16-byte vectors too
 #endif
@@ -810,6 +813,13 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                     if (e0 + 1 >= r_lo && e0 + 1 < r_hi) S.prefetch(x.y);
                     if (e0 + 2 >= r_lo && e0 + 2 < r_hi) S.prefetch(x.z);
                     if (e0 + 3 >= r_lo && e0 + 3 < r_hi) S.prefetch(x.w);
+                } else if (ADSB_PROBE_PREFETCH && S.filt != nullptr) {
+                    // probe passes read the state word only of entries the
+                    // membership filter lets through: those go to L2 together
+                    if (e0 >= r_lo && e0 < r_hi && !S.fmiss(x.x)) S.prefetch(x.x);
+                    if (e0 + 1 >= r_lo && e0 + 1 < r_hi && !S.fmiss(x.y)) S.prefetch(x.y);
+                    if (e0 + 2 >= r_lo && e0 + 2 < r_hi && !S.fmiss(x.z)) S.prefetch(x.z);
+                    if (e0 + 3 >= r_lo && e0 + 3 < r_hi && !S.fmiss(x.w)) S.prefetch(x.w);
                 }
             }
 #pragma unroll 1

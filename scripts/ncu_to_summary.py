@@ -1,6 +1,8 @@
 """Merge one ncu --set full capture of the sampler kernel into profiles/ncu_sampler_summary.json.
 
-    python scripts/ncu_to_summary.py CONFIG REPORT.ncu-rep|RAW.csv SAMPLES_IN_LAUNCH "source note"
+    python scripts/ncu_to_summary.py CONFIG REPORT.ncu-rep|RAW.csv|SUMMARY.json SAMPLES_IN_LAUNCH "source note"
+
+(SUMMARY.json: the output of scripts/ncu_summary.py written on the GPU box.)
 
 Per launch: DRAM bytes (read + write) and L2 bytes (lts__t_bytes), converted
 to bytes per sample, which bench.py scales by the samples a step draws.
@@ -19,7 +21,14 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def metrics(rep: str) -> dict:
-    """rep: an .ncu-rep, or the `ncu -i REP --page raw --csv` output saved on the GPU box"""
+    """rep: an .ncu-rep, the `ncu -i REP --page raw --csv` output saved on the GPU box, or ncu_summary.py's JSON"""
+    if rep.endswith(".json"):
+        d = json.loads(Path(rep).read_text())[0]
+        out = {"kernel": d["kernel"]}
+        for k, v in d.items():
+            if isinstance(v, list):
+                out[k] = v[0] * UNITS.get(v[1], 1.0)
+        return out
     if rep.endswith(".csv"):
         txt = Path(rep).read_text()
     else:
