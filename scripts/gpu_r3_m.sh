@@ -1,0 +1,16 @@
+# Round 2 (session 4) m: lazy level degree sums on the global store only (default build) vs HEAD (head).
+mkdir -p gpurun_out/r3m; rm -f gpurun_out/r3m/*
+export ADSB_GRAPH_CACHE=build/gcache
+for c in c5_rmat24 c2_rmat18 c3_ba; do timeout 300 python -c "
+import sys; sys.path.insert(0,'.')
+from paper_1903_09422_b200 import datasets; datasets.graph('$c')" ; done
+run() { # config, env...
+  c=$1; shift
+  echo "== $c $*" >> gpurun_out/r3m/ab.log
+  env "$@" ADSB_TRACE=1 timeout 300 python scripts/prof_one.py $c 4 2>&1 | grep -E "rep [123]|Error|error" | tail -3 >> gpurun_out/r3m/ab.log
+}
+for i in 1 2 3; do for c in c5_rmat24 c2_rmat18 c3_ba; do run $c ADSB_LIB_PATH=ab/libadsb_head.so; run $c X=1; done; done
+run c5_rmat24 ADSB_NO_SMEM=1 ADSB_LIB_PATH=ab/libadsb_head.so
+run c5_rmat24 ADSB_NO_SMEM=1
+timeout 1800 python -m pytest tests -q -m gpu --timeout 600 -p no:cacheprovider -rf -x > gpurun_out/r3m/pytest.log 2>&1
+echo "pytest exit $?" >> gpurun_out/r3m/pytest.log
