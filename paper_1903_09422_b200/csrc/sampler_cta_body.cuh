@@ -615,6 +615,19 @@ __device__ __forceinline__ uint32_t search_cost(uint32_t deg, bool trees) {
     const uint32_t bits = 32u - __clz(deg);
     return trees && hub_has_tree(deg) ? (bits + 4u) / 3u : bits;
 }
+// adjacency entries one search reads, for the edges_scanned statistic: a
+// binary search reads one entry per step; a tree search reads an 8-key node per
+// level (copies of row entries), the three group ends of the leaf block and
+// three steps inside a group, plus the final comparison
+__device__ __forceinline__ uint32_t search_reads(uint32_t deg, bool trees) {
+    if (!(trees && hub_has_tree(deg))) return 32u - __clz(deg);
+    uint32_t n = (deg + kHubLeaf - 1) / kHubLeaf, levels = 1;
+    while (n > kHubFan) {
+        n = (n + kHubFan - 1) / kHubFan;
+        ++levels;
+    }
+    return kHubFan * levels + 7u;
+}
 // factor in quarters: deg > (factor / 4) |L| cost(deg)
 __device__ __forceinline__ bool is_hub(uint32_t deg, uint32_t list, uint32_t factor, bool trees = false) {
     return ADSB_HUB_PROBE && list && factor &&
@@ -759,7 +772,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                     if constexpr (Store::kTrees)
                         sh.hub_tree[h] = trees && hub_has_tree(e - o) ? __ldg(sh.hub_ref + u) : kNone;
                     nv = 0;
-                    scanned = (l_hi - l_lo) * search_cost(e - o, trees);  // searches, not scans
+                    scanned = (l_hi - l_lo) * search_reads(e - o, trees);  // searches, not scans
                 }
             }
         }
@@ -866,7 +879,7 @@ __device__ void for_edges_tok(Ctx& C, Store& S, uint32_t lo, uint32_t hi, bool t
                     sh.hub_val[h] = val;
                     if constexpr (Store::kTrees)
                         sh.hub_tree[h] = trees && hub_has_tree(deg) ? __ldg(sh.hub_ref + u) : kNone;
-                    hub_reads = (l_hi - l_lo) * search_cost(deg, trees);
+                    hub_reads = (l_hi - l_lo) * search_reads(deg, trees);
                     deg = 0;
                 }
             }
@@ -1515,7 +1528,7 @@ __device__ bool level_pick(Ctx& C, Store& S, uint32_t beg, uint32_t end, uint32_
         uint32_t l = beg, h = end;
         if (Store::kTrees && tree != kNone) {
             l = tree_lower_bound(C, sh.hub_keys + tree, beg, end, q);
-            probes += search_cost(end - beg, true);
+            probes += search_reads(end - beg, true);
         } else {
             while (l < h) {
                 const uint32_t mid = (l + h) >> 1;
