@@ -205,7 +205,11 @@ adsb_status adsb_graph_copy_original_ids(const adsb_graph* g, uint64_t* out) {
     return guard([&] {
         need(g, "graph");
         need(out, "out");
-        std::memcpy(out, g->host.original_ids.data(), g->host.original_ids.size() * sizeof(uint64_t));
+        if (g->host.has_original_ids) {
+            std::memcpy(out, g->host.original_ids.data(), g->host.original_ids.size() * sizeof(uint64_t));
+        } else {  // constructed from dense ids: the identity
+            for (uint32_t v = 0; v < g->host.n; ++v) out[v] = v;
+        }
     });
 }
 

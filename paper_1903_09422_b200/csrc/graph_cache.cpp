@@ -164,8 +164,7 @@ HostGraph load_graph_cache(const std::string& path) {
         g.original_ids.resize(h.n);
         io_section(f.fd, g.original_ids.data(), g.original_ids.size() * 8, off, false, path);
     } else {
-        g.original_ids.resize(h.n);
-        for (uint32_t v = 0; v < h.n; ++v) g.original_ids[v] = v;
+        g.original_ids.clear();  // identity, written on request
     }
     if (graph_hash(g) != h.checksum) parse_error("graph cache '" + path + "' is damaged (checksum mismatch)");
     if (g.offsets[0] != 0 || g.offsets[h.n] != h.nnz) parse_error("graph cache '" + path + "' is damaged (offsets)");

@@ -281,8 +281,7 @@ HostGraph graph_from_edges(uint32_t n, const uint32_t* edges, uint64_t m) {
                         (kept[u + 1] - kept[u]) * sizeof(uint32_t));
     });
     g.offsets.assign(kept.begin(), kept.end());
-    g.original_ids.resize(n);
-    std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});
+    // original_ids stays empty: the identity (has_original_ids == false) is written on request
     return g;
 }
 
@@ -292,8 +291,18 @@ HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nb
 
 HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nbrs, CsrChunkSink* sink) {
     if (offsets[0] != 0) invalid("offsets[0] must be 0");
-    for (uint32_t u = 0; u < n; ++u)
-        if (offsets[u + 1] < offsets[u]) invalid("offsets must be non-decreasing");
+    {
+        // monotone offsets first (the weighted split below searches them), by equal vertex ranges
+        const unsigned T = n >= (1u << 20) ? host_threads() : 1u;
+        std::atomic<bool> decreasing{false};
+        HostPool::get().run(T, [&](unsigned t) {
+            const uint64_t b = static_cast<uint64_t>(n) * t / T, e = static_cast<uint64_t>(n) * (t + 1) / T;
+            bool local = false;
+            for (uint64_t u = b; u < e; ++u) local |= offsets[u + 1] < offsets[u];
+            if (local) decreasing = true;
+        });
+        if (decreasing) invalid("offsets must be non-decreasing");
+    }
     HostGraph g;
     g.n = n;
     g.offsets.resize(static_cast<size_t>(n) + 1);
@@ -318,8 +327,7 @@ HostGraph graph_from_csr(uint32_t n, const uint64_t* offsets, const uint32_t* nb
     });
     g.offsets[n] = offsets[n];
     if (bad) invalid("CSR must have in-range, ascending, duplicate-free, loop-free adjacency");
-    g.original_ids.resize(n);
-    std::iota(g.original_ids.begin(), g.original_ids.end(), uint64_t{0});
+    // original_ids stays empty: the identity (has_original_ids == false) is written on request
     return g;
 }
 

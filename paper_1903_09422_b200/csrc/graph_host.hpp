@@ -62,7 +62,7 @@ struct HostGraph {
     uint32_t n = 0;
     std::vector<uint64_t, NoInitAlloc<uint64_t>> offsets;  // n+1
     std::vector<uint32_t, NoInitAlloc<uint32_t>> nbrs;     // offsets[n], ascending per vertex
-    std::vector<uint64_t> original_ids;  // dense -> id in the input (identity when absent)
+    std::vector<uint64_t> original_ids;  // dense -> id in the input (empty = identity when !has_original_ids)
     bool has_original_ids = false;
 
     uint64_t nnz() const { return nbrs.size(); }
