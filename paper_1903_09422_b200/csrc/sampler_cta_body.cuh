@@ -1132,7 +1132,7 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
     // A claim pass over several times more adjacency than the table has room
     // left fills it: migrate before the pass instead of after (the level's
     // claims run once, on the region). A wrong guess only costs the sample the
-    // slower store. Only the table has a capacity (join_room), and only a
+    // slower store. Only the table has a capacity (table_room), and only a
     // sample that can migrate (io) and is not already resumed takes this exit.
     auto predicted = [&](unsigned long long deg) {
         return ADSB_PREDICT_FACTOR != 0 && io != nullptr && !resume &&
