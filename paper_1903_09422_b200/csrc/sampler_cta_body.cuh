@@ -1073,8 +1073,8 @@ struct BfsState {
 #ifndef ADSB_MIGRATE
 #define ADSB_MIGRATE 1
 #endif
-#ifndef ADSB_PREDICT_FACTOR
-#define ADSB_PREDICT_FACTOR 2  // migrate before a claim pass over more than this x the table's room (0: never)
+#ifndef ADSB_PREDICT_QUARTERS
+#define ADSB_PREDICT_QUARTERS 4  // migrate before a claim pass over more than this / 4 x the table's room (0: never)
 #endif
 
 template <class Store>
@@ -1129,14 +1129,14 @@ __device__ Meet bfs(Ctx& C, Store& S, uint32_t s, uint32_t t, BfsState* io = nul
         if (io) *io = BfsState{s_lo, s_hi, t_lo, t_hi, a, b, used_now, deg_s, deg_t};
         return {a, b, io ? 3 : 1};
     };
-    // A claim pass over several times more adjacency than the table has room
-    // left fills it: migrate before the pass instead of after (the level's
+    // A claim pass over more adjacency than the table has room left (nearly
+    // always) fills it: migrate before the pass instead of after (the level's
     // claims run once, on the region). A wrong guess only costs the sample the
     // slower store. Only the table has a capacity (table_room), and only a
     // sample that can migrate (io) and is not already resumed takes this exit.
     auto predicted = [&](unsigned long long deg) {
-        return ADSB_PREDICT_FACTOR != 0 && io != nullptr && !resume &&
-               deg > static_cast<unsigned long long>(ADSB_PREDICT_FACTOR) * S.table_room(used);
+        return ADSB_PREDICT_QUARTERS != 0 && io != nullptr && !resume &&
+               4ull * deg > static_cast<unsigned long long>(ADSB_PREDICT_QUARTERS) * S.table_room(used);
     };
     for (;;) {
         const bool skip_probe = skip_next;  // first level of a resumed sample: its probe already ran
